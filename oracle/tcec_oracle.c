@@ -1,0 +1,368 @@
+/*
+ * tcec_oracle.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * CPU restatement of the reference's error-corrected GEMM path
+ * (/root/reference/pkg/src/tcgemm), used exclusively as the parity CHECKER by
+ * tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+ * reference legs.  Nothing in the product package links, loads or calls this
+ * file: the product path is the sm_100a CUDA library built from
+ * paper_2203_03341_b200/csrc.
+ *
+ * Parity pin: the restatement is checked bit-for-bit against golden vectors
+ * produced by importing the reference package in the build container
+ * (tests/golden/make_golden.py -> tests/golden/ fixtures, tests/test_oracle_golden.py).
+ *
+ * Every function cites the reference lines it restates.  All arithmetic runs in
+ * IEEE binary64 (the reference's float64 carrier) and must be compiled without
+ * -ffast-math and with -ffp-contract=off so that the TwoSum error-free
+ * transformation is not contracted.
+ */
+#include <math.h>
+#include <pthread.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <unistd.h>
+
+enum { FMT_FP16 = 0, FMT_TF32 = 1, FMT_FP32 = 2 };
+enum { RM_RN = 0, RM_RNA = 1, RM_RZ = 2 };
+
+#define ORACLE_FLAG_OVERFLOW 1u
+#define ORACLE_FLAG_OUT_OF_RANGE 2u
+
+typedef struct {
+  int man_bits;
+  int min_normal_exp;
+  int max_normal_exp;
+  double max_finite;
+} fmt_t;
+
+/* formats.py:107-111 (FP16/TF32/FP32 constants) and :84-104 (derived limits). */
+static fmt_t fmt_of(int f) {
+  fmt_t r;
+  if (f == FMT_FP16) {
+    r.man_bits = 10; r.min_normal_exp = -14; r.max_normal_exp = 15;
+  } else if (f == FMT_TF32) {
+    r.man_bits = 10; r.min_normal_exp = -126; r.max_normal_exp = 127;
+  } else {
+    r.man_bits = 23; r.min_normal_exp = -126; r.max_normal_exp = 127;
+  }
+  r.max_finite = ldexp(2.0 - ldexp(1.0, -r.man_bits), r.max_normal_exp);
+  return r;
+}
+
+/* formats.py:114-142 (_round_general): quantum at the value's binade (pinned at
+ * the smallest subnormal below the normal range), floor + tie rule, RZ
+ * saturates to max_finite, RN/RNA overflow to +-inf. */
+static double round_general(double x, int f, int mode) {
+  if (!isfinite(x)) return x;
+  fmt_t F = fmt_of(f);
+  double a = fabs(x);
+  int e2;
+  (void)frexp(a, &e2);
+  int e = e2 - 1;
+  int qe = (e > F.min_normal_exp ? e : F.min_normal_exp) - F.man_bits;
+  double q = ldexp(1.0, qe);
+  double n = a / q;
+  double lo = floor(n);
+  double frac = n - lo;
+  double k;
+  if (mode == RM_RZ) {
+    k = lo;
+  } else if (mode == RM_RNA) {
+    k = lo + (frac >= 0.5 ? 1.0 : 0.0);
+  } else {
+    int odd = fmod(lo, 2.0) != 0.0;
+    k = lo + (((frac > 0.5) || (frac == 0.5 && odd)) ? 1.0 : 0.0);
+  }
+  double r = k * q;
+  if (mode == RM_RZ) {
+    r = r < F.max_finite ? r : F.max_finite;
+  } else if (r > F.max_finite) {
+    r = INFINITY;
+  }
+  return copysign(r, x);
+}
+
+/* formats.py:145-167 (round_to_format): RN to FP32 / FP16 use correctly
+ * rounded binary casts (numpy astype(float32) / astype(float16)); every other
+ * (format, mode) pair goes through _round_general. */
+static double round_to_format(double x, int f, int mode) {
+  if (mode == RM_RN && f == FMT_FP32) return (double)(float)x;
+  if (mode == RM_RN && f == FMT_FP16) return (double)(_Float16)x;
+  return round_general(x, f, mode);
+}
+
+/* formats.py:170-176 (_truncate_raw): sign-magnitude RZ to `bits` significand
+ * bits at the value's own binade; exponent range unbounded.  For normal
+ * binary64 values this is a mask of the low (53 - bits) stored bits, which is
+ * bit-identical to the frexp / trunc / ldexp formulation used for the rest. */
+static inline double truncate_raw(double x, int bits) {
+  uint64_t u;
+  memcpy(&u, &x, 8);
+  uint64_t ex = u & 0x7FF0000000000000ull;
+  if (ex != 0 && ex != 0x7FF0000000000000ull) {
+    u &= ~((1ull << (53 - bits)) - 1ull);
+    memcpy(&x, &u, 8);
+    return x;
+  }
+  int e;
+  double m = frexp(x, &e);
+  double nn = trunc(ldexp(m, bits));
+  return ldexp(nn, e - bits);
+}
+
+/* mma.py:48-62 (_sum_round_to_odd): TwoSum, then force the last significand
+ * bit odd when the sum is inexact, so that any later rounding to <= 51 bits
+ * equals rounding the exact sum.  The parity test reads the stored LSB for
+ * normal binary64 (identical to fmod(ldexp(frexp(s), 53), 2)) and falls back
+ * to the literal formulation otherwise. */
+static inline double sum_round_to_odd(double a, double b) {
+  double s = a + b;
+  double tmp = s - a;
+  double err = (a - (s - tmp)) + (b - tmp);
+  if (err != 0.0 && isfinite(s)) {
+    uint64_t u;
+    memcpy(&u, &s, 8);
+    int even;
+    if ((u & 0x7FF0000000000000ull) != 0) {
+      even = (u & 1ull) == 0;
+    } else {
+      int e;
+      double m = frexp(s, &e);
+      even = fmod(ldexp(m, 53), 2.0) == 0.0;
+    }
+    if (even) s = nextafter(s, err > 0.0 ? INFINITY : -INFINITY);
+  }
+  return s;
+}
+
+/* round_to_format(., FP32, RZ) (formats.py:114-142) specialised: inside the
+ * FP32 normal range it is a 24-bit truncation (mask of 29 stored bits). */
+static inline double rz32(double x) {
+  uint64_t u;
+  memcpy(&u, &x, 8);
+  int be = (int)((u >> 52) & 0x7FF) - 1023;
+  if (be >= -126 && be <= 127) {
+    u &= ~((1ull << 29) - 1ull);
+    memcpy(&x, &u, 8);
+    return x;
+  }
+  return round_general(x, FMT_FP32, RM_RZ);
+}
+
+/* schemes.py:174-175 (_round32_rn). */
+static inline double rn32(double x) { return (double)(float)x; }
+
+/* splitting.py:114-122 (_split_arrays): hi = round(x); residual = (x - hi) *
+ * 2^s exactly (carrier); lo = round(residual); lo = 0 where hi overflowed. */
+static void split_one(double x, int f, int s, int mode, double *hi, double *lo) {
+  double h = round_to_format(x, f, mode);
+  double hh = isfinite(h) ? h : x;
+  double res = ldexp(x - hh, s);
+  double l = round_to_format(res, f, mode);
+  *hi = h;
+  *lo = isfinite(h) ? l : 0.0;
+}
+
+/* splitting.py:187-215 (classify_array): 0 high precision, 1 degraded,
+ * 2 out of range. */
+static int classify_one(double x, int f, int s) {
+  if (x == 0.0) return 0;
+  int e2;
+  (void)frexp(fabs(x), &e2);
+  int ev = e2 - 1;
+  int degraded, oor;
+  if (f == FMT_TF32) {
+    degraded = ev < -126 + 23;
+    oor = (ev < -126) || (ev > 127);
+  } else {
+    degraded = ev < -15;
+    oor = (ev + s <= -24) || (ev > 15);
+  }
+  return oor ? 2 : (degraded ? 1 : 0);
+}
+
+/* ------------------------------------------------------------------ API -- */
+
+int tcec_oracle_version(void) { return 1; }
+
+int tcec_oracle_round(int f, int mode, int64_t count, const double *x, double *out) {
+  for (int64_t i = 0; i < count; ++i) out[i] = round_to_format(x[i], f, mode);
+  return 0;
+}
+
+int tcec_oracle_split(int f, int s, int mode, int64_t count, const float *x, double *hi,
+                      double *lo) {
+  for (int64_t i = 0; i < count; ++i) split_one((double)x[i], f, s, mode, &hi[i], &lo[i]);
+  return 0;
+}
+
+int tcec_oracle_classify(int f, int s, int64_t count, const float *x, int8_t *out) {
+  for (int64_t i = 0; i < count; ++i) out[i] = (int8_t)classify_one((double)x[i], f, s);
+  return 0;
+}
+
+typedef struct {
+  /* split operands, row-contiguous along (padded) k */
+  const double *ah, *al; /* m x kp */
+  const double *bh, *bl; /* n x kp (B transposed) */
+  int64_t m, n, kp;
+  float *C;
+  int64_t ldc;
+  int f, s, bk, drain, acc_bits, include_dd;
+  int64_t row_begin, row_end;
+  int nonfinite_out;
+} job_t;
+
+/* schemes.py:265-314 (_corrected_core), per output element.  Per k-block the
+ * residual chain receives dA*B then A*dB (terminal RZ each, mma.py:84-85),
+ * the main term is accumulated in a 25-bit RZ unit (mma.py:65-81) from a zero
+ * fragment and folded into C with one FP32 RN add.  `drain` > block_k is the
+ * drain-interval restatement of SURVEY.md Appendix A (composed of the same
+ * primitives): the main fragment takes a terminal RZ per block and is folded
+ * into C every drain/block_k blocks; drain == block_k is the reference. */
+static void *corrected3_rows(void *arg) {
+  job_t *J = (job_t *)arg;
+  const int64_t nb = J->kp / J->bk;
+  const int64_t bpg = J->drain / J->bk;
+  const double scale = ldexp(1.0, -J->s);
+  const double scale2 = ldexp(1.0, -2 * J->s);
+  for (int64_t i = J->row_begin; i < J->row_end; ++i) {
+    const double *ah = J->ah + i * J->kp, *al = J->al + i * J->kp;
+    for (int64_t j = 0; j < J->n; ++j) {
+      const double *bh = J->bh + j * J->kp, *bl = J->bl + j * J->kp;
+      double dc = 0.0, ddc = 0.0, c = 0.0, tmpg = 0.0;
+      for (int64_t b = 0; b < nb; ++b) {
+        double a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0;
+        const int64_t t0 = b * J->bk, t1 = t0 + J->bk;
+        for (int64_t t = t0; t < t1; ++t) {
+          a1 = truncate_raw(sum_round_to_odd(a1, al[t] * bh[t]), J->acc_bits);
+          a2 = truncate_raw(sum_round_to_odd(a2, ah[t] * bl[t]), J->acc_bits);
+          a3 = truncate_raw(sum_round_to_odd(a3, ah[t] * bh[t]), J->acc_bits);
+          if (J->include_dd)
+            a4 = truncate_raw(sum_round_to_odd(a4, al[t] * bl[t]), J->acc_bits);
+        }
+        dc = rz32(sum_round_to_odd(a1, dc));
+        dc = rz32(sum_round_to_odd(a2, dc));
+        if (J->include_dd) ddc = rz32(sum_round_to_odd(a4, ddc));
+        tmpg = rz32(sum_round_to_odd(a3, tmpg));
+        if ((b + 1) % bpg == 0 || b == nb - 1) {
+          c = rn32(sum_round_to_odd(c, tmpg));
+          tmpg = 0.0;
+        }
+      }
+      c = rn32(sum_round_to_odd(c, dc * scale));
+      if (J->include_dd) c = rn32(sum_round_to_odd(c, ddc * scale2));
+      float cf = (float)c;
+      if (!isfinite(cf)) J->nonfinite_out = 1;
+      J->C[i * J->ldc + j] = cf;
+    }
+  }
+  return NULL;
+}
+
+static int resolve_threads(int nthreads) {
+  if (nthreads > 0) return nthreads;
+  long p = sysconf(_SC_NPROCESSORS_ONLN);
+  return p > 0 ? (int)p : 1;
+}
+
+/* schemes.py:317-373 (gemm, corrected3 branch) + :210-218 (_pad_k) +
+ * :237-241 (_split_flags) + :369-371 (overflow on non-finite output).
+ * Returns 0 on success, negative on bad arguments or allocation failure. */
+int tcec_oracle_corrected3(int f, int s, int mode, int64_t m, int64_t n, int64_t k,
+                           const float *A, int64_t lda, const float *B, int64_t ldb,
+                           float *C, int64_t ldc, int block_k, int drain_k, int acc_bits,
+                           int include_dd, int nthreads, uint32_t *flags) {
+  if (m < 0 || n < 0 || k < 0 || block_k < 1 || drain_k < block_k || drain_k % block_k)
+    return -1;
+  if (acc_bits < 1 || acc_bits > 53) return -1;
+  const int64_t kp = ((k + block_k - 1) / block_k) * block_k;
+  double *ah = calloc((size_t)(m * kp + 1), sizeof(double));
+  double *al = calloc((size_t)(m * kp + 1), sizeof(double));
+  double *bh = calloc((size_t)(n * kp + 1), sizeof(double));
+  double *bl = calloc((size_t)(n * kp + 1), sizeof(double));
+  if (!ah || !al || !bh || !bl) {
+    free(ah); free(al); free(bh); free(bl);
+    return -2;
+  }
+  uint32_t fl = 0;
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t t = 0; t < k; ++t) {
+      double x = (double)A[i * lda + t];
+      split_one(x, f, s, mode, &ah[i * kp + t], &al[i * kp + t]);
+      if (isinf(ah[i * kp + t])) fl |= ORACLE_FLAG_OVERFLOW;
+      if (classify_one(x, f, s) == 2) fl |= ORACLE_FLAG_OUT_OF_RANGE;
+    }
+  for (int64_t t = 0; t < k; ++t)
+    for (int64_t j = 0; j < n; ++j) {
+      double x = (double)B[t * ldb + j];
+      split_one(x, f, s, mode, &bh[j * kp + t], &bl[j * kp + t]);
+      if (isinf(bh[j * kp + t])) fl |= ORACLE_FLAG_OVERFLOW;
+      if (classify_one(x, f, s) == 2) fl |= ORACLE_FLAG_OUT_OF_RANGE;
+    }
+  int nt = resolve_threads(nthreads);
+  if (nt > m && m > 0) nt = (int)m;
+  if (nt < 1) nt = 1;
+  job_t *jobs = calloc((size_t)nt, sizeof(job_t));
+  pthread_t *th = calloc((size_t)nt, sizeof(pthread_t));
+  int64_t per = (m + nt - 1) / nt;
+  for (int w = 0; w < nt; ++w) {
+    job_t *J = &jobs[w];
+    J->ah = ah; J->al = al; J->bh = bh; J->bl = bl;
+    J->m = m; J->n = n; J->kp = kp; J->C = C; J->ldc = ldc;
+    J->f = f; J->s = s; J->bk = block_k; J->drain = drain_k; J->acc_bits = acc_bits;
+    J->include_dd = include_dd;
+    J->row_begin = w * per;
+    J->row_end = (w + 1) * per < m ? (w + 1) * per : m;
+    if (J->row_begin > m) J->row_begin = m;
+    if (nt == 1) corrected3_rows(J);
+    else pthread_create(&th[w], NULL, corrected3_rows, J);
+  }
+  if (nt > 1)
+    for (int w = 0; w < nt; ++w) pthread_join(th[w], NULL);
+  for (int w = 0; w < nt; ++w)
+    if (jobs[w].nonfinite_out) fl |= ORACLE_FLAG_OVERFLOW;
+  free(jobs); free(th);
+  free(ah); free(al); free(bh); free(bl);
+  if (flags) *flags = fl;
+  return 0;
+}
+
+/* schemes.py:187-202 (_blocked_simt32): FP32 RN products and sums, ascending
+ * k, a fresh partial per block folded into the carried sum. */
+int tcec_oracle_fp32_simt(int64_t m, int64_t n, int64_t k, const float *A, int64_t lda,
+                          const float *B, int64_t ldb, float *C, int64_t ldc, int block_k) {
+  if (block_k < 1) return -1;
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t j = 0; j < n; ++j) {
+      float acc = 0.0f;
+      for (int64_t s0 = 0; s0 < k; s0 += block_k) {
+        float part = 0.0f;
+        int64_t s1 = s0 + block_k < k ? s0 + block_k : k;
+        for (int64_t t = s0; t < s1; ++t) {
+          volatile float p = A[i * lda + t] * B[t * ldb + j];
+          part = part + p;
+        }
+        acc = acc + part;
+      }
+      C[i * ldc + j] = acc;
+    }
+  return 0;
+}
+
+/* schemes.py:178-184 (_sequential_ref64): binary64 RN, ascending k. */
+int tcec_oracle_fp64_ref(int64_t m, int64_t n, int64_t k, const float *A, int64_t lda,
+                         const float *B, int64_t ldb, double *C, int64_t ldc) {
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t j = 0; j < n; ++j) {
+      double acc = 0.0;
+      for (int64_t t = 0; t < k; ++t) {
+        volatile double p = (double)A[i * lda + t] * (double)B[t * ldb + j];
+        acc = acc + p;
+      }
+      C[i * ldc + j] = acc;
+    }
+  return 0;
+}
