@@ -1,0 +1,105 @@
+/*
+ * tcec.h -- C ABI of the B200 (sm_100a) error-corrected single-precision GEMM
+ * (Ootomo & Yokota, arXiv 2203.03341: FP16-TCEC and TF32-TCEC).
+ *
+ * This is the drop-in boundary for the reference's GEMM entry point
+ * (reference: /root/reference/pkg/src/tcgemm/schemes.py).  Plain pointers and
+ * sizes only; no framework types.  Every entry point is reentrant and
+ * stream-ordered; results are deterministic (no atomics in any reduction of C).
+ *
+ * Library: paper_2203_03341_b200/libtcec.so (nvcc, -gencode arch=compute_100a,code=sm_100a).
+ */
+#ifndef TCEC_H_
+#define TCEC_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Variants: the two corrected3 schemes of the reference registry
+ * (schemes.py:135-136 "corrected3_halfhalf" / "corrected3_tf32";
+ * split recipes splitting.py:70-79 scaled_halfhalf() / tf32tf32()). */
+#define TCEC_FP16 0 /* FP16-TCEC: hi/lo in FP16, residual scaled by 2^11 */
+#define TCEC_TF32 1 /* TF32-TCEC: hi/lo in TF32, no residual scaling      */
+
+/* Split rounding modes (formats.py:43-55 RoundingMode). */
+#define TCEC_ROUND_DEFAULT (-1) /* RN for FP16, RNA for TF32 (splitting.py:50-59) */
+#define TCEC_ROUND_RN 0
+#define TCEC_ROUND_RNA 1 /* TF32 only */
+#define TCEC_ROUND_RZ 2
+
+/* Device flag bits (RunFlags, schemes.py:140-143). */
+#define TCEC_FLAG_OVERFLOW 1u     /* some hi overflowed, or some output non-finite */
+#define TCEC_FLAG_OUT_OF_RANGE 2u /* some input outside the split's representable band */
+#define TCEC_FLAG_NONFINITE_INPUT 4u /* some input is inf or NaN (the reference raises) */
+
+/* Status codes. */
+#define TCEC_OK 0
+#define TCEC_ERR_ARG (-1)         /* bad shape / leading dimension / option      */
+#define TCEC_ERR_ALIGN (-2)       /* pointer or leading dimension not 16-B aligned */
+#define TCEC_ERR_UNSUPPORTED (-3) /* variant/rounding/drain combination not built  */
+#define TCEC_ERR_CUDA (-4)        /* CUDA runtime / driver error                   */
+#define TCEC_ERR_ARCH (-5)        /* current device is not sm_100                  */
+
+typedef struct tcec_opts {
+  /* Split rounding (TCEC_ROUND_*); replaces SplitScheme.rounding. */
+  int32_t split_rounding;
+  /* log2 of the residual scale: -1 = scheme default (11 FP16, 0 TF32);
+   * 0 with FP16 is the unscaled markidis_halfhalf split (splitting.py:70-71). */
+  int32_t scale_log2;
+  /* Drain interval of the main-term partial in k (MmaConfig.block_k,
+   * mma.py:34): 0 = one operand stage (64 for FP16, 32 for TF32); otherwise a
+   * positive multiple of that stage depth. */
+  int32_t drain_k;
+  /* Output tile width: 0 = default (128). */
+  int32_t block_n;
+  /* Tile rasterisation group along m: 0 = default (16). */
+  int32_t group_m;
+  int32_t reserved[3];
+} tcec_opts;
+
+/* Library version (major * 10000 + minor * 100 + patch). */
+int tcec_version(void);
+
+/* Human-readable text for a status code. */
+const char* tcec_status_str(int status);
+
+/* C = A * B with the corrected3 scheme.  Replaces
+ *   tcgemm.gemm(a, b, SCHEMES_BY_NAME["corrected3_halfhalf" | "corrected3_tf32"], cfg)
+ * (schemes.py:317-373; core _corrected_core :265-314).
+ * A: m x k, row-major, leading dimension lda (>= k) -- device pointer
+ * B: k x n, row-major, leading dimension ldb (>= n) -- device pointer
+ * C: m x n, row-major, leading dimension ldc (>= n) -- device pointer, written
+ * Pointers must be 16-byte aligned and lda/ldb/ldc multiples of 4 (TMA).
+ * opts may be NULL (defaults).  d_flags (device uint32, may be NULL) is OR-ed
+ * with TCEC_FLAG_* bits (the caller zeroes it).  stream is a cudaStream_t.
+ * k == 0 writes zeros; m == 0 or n == 0 is a no-op. */
+int tcec_sgemm(int variant, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda,
+               const float* B, int64_t ldb, float* C, int64_t ldc, const tcec_opts* opts,
+               uint32_t* d_flags, void* stream);
+
+/* Same computation on HOST buffers (the numpy-facing binding): copies A and B
+ * to the device, runs tcec_sgemm, copies C back and synchronises the stream.
+ * Host buffers may be pageable; pinned buffers copy faster.  h_flags may be
+ * NULL.  Row-major, leading dimensions as above (no alignment requirement). */
+int tcec_sgemm_host(int variant, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda,
+                    const float* B, int64_t ldb, float* C, int64_t ldc, const tcec_opts* opts,
+                    uint32_t* h_flags, void* stream);
+
+/* Elementwise split of count FP32 values (splitting.py:114-122 _split_arrays,
+ * split_matrix :139-147): hi and lo are written as FP32 values (FP16 values
+ * widened exactly).  d_flags as above (classify_array :187-215).  Device
+ * pointers, 4-byte aligned. */
+int tcec_split(int variant, int rounding, int scale_log2, const float* X, int64_t count,
+               float* hi, float* lo, uint32_t* d_flags, void* stream);
+
+/* Number of kernel launches issued by this library since load (diagnostic). */
+uint64_t tcec_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TCEC_H_ */

@@ -1,0 +1,301 @@
+// tcec_capi.cu -- host side of the C ABI declared in include/tcec.h.
+//
+// Validation mirrors the reference's gemm() contract (schemes.py:163-171,
+// :327-330): shape errors are reported, numerical anomalies only raise flags.
+// Tensor maps are encoded per call through the driver entry point obtained
+// from the runtime (no link-time libcuda dependency).
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include "tcec.h"
+#include "tcec_gemm.cuh"
+
+namespace {
+
+std::atomic<uint64_t> g_launches{0};
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_encode_once;
+int g_encode_status = TCEC_ERR_CUDA;
+
+int get_encoder() {
+  std::call_once(g_encode_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess && fn != nullptr) {
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+      g_encode_status = TCEC_OK;
+    }
+  });
+  return g_encode_status;
+}
+
+int check_arch() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return TCEC_ERR_CUDA;
+  int major = 0, minor = 0;
+  if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess)
+    return TCEC_ERR_CUDA;
+  return (major == 10 && minor == 0) ? TCEC_OK : TCEC_ERR_ARCH;
+}
+
+// 2-D fp32 tensor map over a row-major [outer][inner] matrix.
+int make_tmap(CUtensorMap* tm, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld_elems,
+              uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle swz) {
+  const cuuint64_t dims[2] = {inner, outer};
+  const cuuint64_t strides[1] = {ld_elems * sizeof(float)};
+  const cuuint32_t box[2] = {box_inner, box_outer};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims,
+                              strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? TCEC_OK : TCEC_ERR_CUDA;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+template <int V, int R, int BN>
+int launch_gemm(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, const float* B,
+                int64_t ldb, float* C, int64_t ldc, int scale_log2, int drain_every, int group_m,
+                uint32_t* d_flags, cudaStream_t stream) {
+  using Cfg = tcec::TileCfg<BN>;
+  using VC = tcec::VarCfg<V>;
+  CUtensorMap tmA, tmB, tmC;
+  int st;
+  if ((st = make_tmap(&tmA, A, k, m, lda, Cfg::BK_STG, Cfg::BM, CU_TENSOR_MAP_SWIZZLE_128B)))
+    return st;
+  if ((st = make_tmap(&tmB, B, n, k, ldb, BN, Cfg::BK_STG, CU_TENSOR_MAP_SWIZZLE_NONE))) return st;
+  if ((st = make_tmap(&tmC, C, n, m, ldc, Cfg::EPI_BOX, Cfg::EPI_BOX, CU_TENSOR_MAP_SWIZZLE_128B)))
+    return st;
+
+  auto kern = tcec::tcec_gemm_kernel<V, R, BN>;
+  static std::once_flag attr_once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(attr_once, [&] {
+    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    Cfg::SMEM_BYTES);
+  });
+  if (attr_err != cudaSuccess) return TCEC_ERR_CUDA;
+
+  tcec::GemmShape shp;
+  shp.m = static_cast<int32_t>(m);
+  shp.n = static_cast<int32_t>(n);
+  shp.k = static_cast<int32_t>(k);
+  shp.num_op_stages = static_cast<int32_t>((k + VC::BK_OP - 1) / VC::BK_OP);
+  shp.drain_every = drain_every;
+  shp.group_m = group_m;
+  const float scale = ldexpf(1.0f, scale_log2);
+  const float inv_scale = ldexpf(1.0f, -scale_log2);
+  const tcec::FlagThresholds thr = tcec::flag_thresholds(V, R, scale_log2);
+  const int64_t tiles = ((m + Cfg::BM - 1) / Cfg::BM) * ((n + BN - 1) / BN);
+  kern<<<static_cast<unsigned>(tiles), Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream>>>(
+      tmA, tmB, tmC, shp, scale, inv_scale, thr, d_flags);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError() == cudaSuccess ? TCEC_OK : TCEC_ERR_CUDA;
+}
+
+template <int V, int R>
+int dispatch_bn(int bn, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda,
+                const float* B, int64_t ldb, float* C, int64_t ldc, int s, int de, int gm,
+                uint32_t* fl, cudaStream_t st) {
+  switch (bn) {
+    case 128:
+      return launch_gemm<V, R, 128>(m, n, k, A, lda, B, ldb, C, ldc, s, de, gm, fl, st);
+    default:
+      return TCEC_ERR_UNSUPPORTED;
+  }
+}
+
+int resolve_rounding(int variant, int rounding) {
+  if (rounding == TCEC_ROUND_DEFAULT) return variant == TCEC_FP16 ? TCEC_ROUND_RN : TCEC_ROUND_RNA;
+  return rounding;
+}
+
+template <int V, int R>
+int launch_split(const float* X, int64_t count, int scale_log2, float* hi, float* lo,
+                 uint32_t* d_flags, cudaStream_t stream) {
+  const float scale = ldexpf(1.0f, scale_log2);
+  const tcec::FlagThresholds thr = tcec::flag_thresholds(V, R, scale_log2);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t pairs = (count + 1) / 2;
+  int64_t blocks = (pairs + 255) / 256;
+  const int64_t cap = static_cast<int64_t>(sms) * 16;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  tcec::tcec_split_kernel<V, R><<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
+      X, count, scale, thr, hi, lo, d_flags);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError() == cudaSuccess ? TCEC_OK : TCEC_ERR_CUDA;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tcec_version(void) { return 100; }
+
+uint64_t tcec_launch_count(void) { return g_launches.load(); }
+
+const char* tcec_status_str(int status) {
+  switch (status) {
+    case TCEC_OK: return "ok";
+    case TCEC_ERR_ARG: return "invalid argument (shape, leading dimension or option)";
+    case TCEC_ERR_ALIGN: return "pointer or leading dimension not 16-byte aligned";
+    case TCEC_ERR_UNSUPPORTED: return "unsupported variant / rounding / drain / tile option";
+    case TCEC_ERR_CUDA: return "CUDA error";
+    case TCEC_ERR_ARCH: return "current device is not an sm_100 (B200) GPU";
+    default: return "unknown status";
+  }
+}
+
+int tcec_sgemm(int variant, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda,
+               const float* B, int64_t ldb, float* C, int64_t ldc, const tcec_opts* opts,
+               uint32_t* d_flags, void* stream) {
+  if (variant != TCEC_FP16 && variant != TCEC_TF32) return TCEC_ERR_ARG;
+  if (m < 0 || n < 0 || k < 0) return TCEC_ERR_ARG;
+  if (m > INT32_MAX || n > INT32_MAX || k > INT32_MAX) return TCEC_ERR_ARG;
+  if (lda < (k > 0 ? k : 1) || ldb < (n > 0 ? n : 1) || ldc < (n > 0 ? n : 1)) return TCEC_ERR_ARG;
+  tcec_opts o;
+  memset(&o, 0, sizeof(o));
+  o.split_rounding = TCEC_ROUND_DEFAULT;
+  o.scale_log2 = -1;
+  if (opts) o = *opts;
+  const int rounding = resolve_rounding(variant, o.split_rounding);
+  int scale_log2 = o.scale_log2 < 0 ? (variant == TCEC_FP16 ? 11 : 0) : o.scale_log2;
+  if (variant == TCEC_TF32 && scale_log2 != 0) return TCEC_ERR_UNSUPPORTED;
+  if (variant == TCEC_FP16 && scale_log2 != 0 && scale_log2 != 11) return TCEC_ERR_UNSUPPORTED;
+  const int bk_op = variant == TCEC_FP16 ? 64 : 32;
+  int drain_every = 1;
+  if (o.drain_k != 0) {
+    if (o.drain_k < 0 || o.drain_k % bk_op != 0) return TCEC_ERR_UNSUPPORTED;
+    drain_every = o.drain_k / bk_op;
+  }
+  const int block_n = o.block_n == 0 ? 128 : o.block_n;
+  const int group_m = o.group_m <= 0 ? 16 : o.group_m;
+  if (m == 0 || n == 0) return TCEC_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (k == 0) {
+    // schemes.py:210-218 + 300-307 with zero blocks: C = 0 exactly
+    return cudaMemset2DAsync(C, ldc * sizeof(float), 0, n * sizeof(float), m, st) == cudaSuccess
+               ? TCEC_OK
+               : TCEC_ERR_CUDA;
+  }
+  if (!aligned16(A) || !aligned16(B) || !aligned16(C) || (lda % 4) || (ldb % 4) || (ldc % 4))
+    return TCEC_ERR_ALIGN;
+  int s;
+  if ((s = check_arch())) return s;
+  if ((s = get_encoder())) return s;
+  if (variant == TCEC_FP16) {
+    if (rounding == TCEC_ROUND_RN)
+      return dispatch_bn<tcec::kFP16, tcec::kRN>(block_n, m, n, k, A, lda, B, ldb, C, ldc,
+                                                 scale_log2, drain_every, group_m, d_flags, st);
+    if (rounding == TCEC_ROUND_RZ)
+      return dispatch_bn<tcec::kFP16, tcec::kRZ>(block_n, m, n, k, A, lda, B, ldb, C, ldc,
+                                                 scale_log2, drain_every, group_m, d_flags, st);
+    return TCEC_ERR_UNSUPPORTED;
+  }
+  if (rounding == TCEC_ROUND_RNA)
+    return dispatch_bn<tcec::kTF32, tcec::kRNA>(block_n, m, n, k, A, lda, B, ldb, C, ldc, 0,
+                                                drain_every, group_m, d_flags, st);
+  if (rounding == TCEC_ROUND_RN)
+    return dispatch_bn<tcec::kTF32, tcec::kRN>(block_n, m, n, k, A, lda, B, ldb, C, ldc, 0,
+                                               drain_every, group_m, d_flags, st);
+  if (rounding == TCEC_ROUND_RZ)
+    return dispatch_bn<tcec::kTF32, tcec::kRZ>(block_n, m, n, k, A, lda, B, ldb, C, ldc, 0,
+                                               drain_every, group_m, d_flags, st);
+  return TCEC_ERR_UNSUPPORTED;
+}
+
+int tcec_sgemm_host(int variant, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda,
+                    const float* B, int64_t ldb, float* C, int64_t ldc, const tcec_opts* opts,
+                    uint32_t* h_flags, void* stream) {
+  if (m < 0 || n < 0 || k < 0) return TCEC_ERR_ARG;
+  if (lda < (k > 0 ? k : 1) || ldb < (n > 0 ? n : 1) || ldc < (n > 0 ? n : 1)) return TCEC_ERR_ARG;
+  if (h_flags) *h_flags = 0;
+  if (m == 0 || n == 0) return TCEC_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // device copies with 16-byte aligned rows
+  const int64_t dlda = ((k > 0 ? k : 1) + 3) / 4 * 4;
+  const int64_t dldb = (n + 3) / 4 * 4;
+  const int64_t dldc = dldb;
+  float *dA = nullptr, *dB = nullptr, *dC = nullptr;
+  uint32_t* dF = nullptr;
+  int status = TCEC_OK;
+  auto cu = [&](cudaError_t e) {
+    if (e != cudaSuccess && status == TCEC_OK) status = TCEC_ERR_CUDA;
+    return e == cudaSuccess;
+  };
+  const size_t bytesA = static_cast<size_t>(m) * dlda * sizeof(float);
+  const size_t bytesB = static_cast<size_t>(k > 0 ? k : 1) * dldb * sizeof(float);
+  const size_t bytesC = static_cast<size_t>(m) * dldc * sizeof(float);
+  if (cu(cudaMallocAsync(reinterpret_cast<void**>(&dA), bytesA, st)) &&
+      cu(cudaMallocAsync(reinterpret_cast<void**>(&dB), bytesB, st)) &&
+      cu(cudaMallocAsync(reinterpret_cast<void**>(&dC), bytesC, st)) &&
+      cu(cudaMallocAsync(reinterpret_cast<void**>(&dF), sizeof(uint32_t), st)) &&
+      cu(cudaMemsetAsync(dF, 0, sizeof(uint32_t), st))) {
+    bool ok = true;
+    if (k > 0) {
+      ok = cu(cudaMemcpy2DAsync(dA, dlda * sizeof(float), A, lda * sizeof(float),
+                                k * sizeof(float), m, cudaMemcpyHostToDevice, st)) &&
+           cu(cudaMemcpy2DAsync(dB, dldb * sizeof(float), B, ldb * sizeof(float),
+                                n * sizeof(float), k, cudaMemcpyHostToDevice, st));
+    }
+    if (ok) {
+      const int s = tcec_sgemm(variant, m, n, k, dA, dlda, dB, dldb, dC, dldc, opts, dF, st);
+      if (s != TCEC_OK) status = s;
+    }
+    if (status == TCEC_OK) {
+      cu(cudaMemcpy2DAsync(C, ldc * sizeof(float), dC, dldc * sizeof(float), n * sizeof(float), m,
+                           cudaMemcpyDeviceToHost, st));
+      if (h_flags) cu(cudaMemcpyAsync(h_flags, dF, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    }
+  }
+  if (dA) cudaFreeAsync(dA, st);
+  if (dB) cudaFreeAsync(dB, st);
+  if (dC) cudaFreeAsync(dC, st);
+  if (dF) cudaFreeAsync(dF, st);
+  cu(cudaStreamSynchronize(st));
+  return status;
+}
+
+int tcec_split(int variant, int rounding, int scale_log2, const float* X, int64_t count,
+               float* hi, float* lo, uint32_t* d_flags, void* stream) {
+  if (variant != TCEC_FP16 && variant != TCEC_TF32) return TCEC_ERR_ARG;
+  if (count < 0) return TCEC_ERR_ARG;
+  if (count == 0) return TCEC_OK;
+  rounding = resolve_rounding(variant, rounding);
+  if (scale_log2 < 0) scale_log2 = variant == TCEC_FP16 ? 11 : 0;
+  if (variant == TCEC_TF32 && scale_log2 != 0) return TCEC_ERR_UNSUPPORTED;
+  if (variant == TCEC_FP16 && scale_log2 != 0 && scale_log2 != 11) return TCEC_ERR_UNSUPPORTED;
+  int s;
+  if ((s = check_arch())) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (variant == TCEC_FP16) {
+    if (rounding == TCEC_ROUND_RN)
+      return launch_split<tcec::kFP16, tcec::kRN>(X, count, scale_log2, hi, lo, d_flags, st);
+    if (rounding == TCEC_ROUND_RZ)
+      return launch_split<tcec::kFP16, tcec::kRZ>(X, count, scale_log2, hi, lo, d_flags, st);
+    return TCEC_ERR_UNSUPPORTED;
+  }
+  if (rounding == TCEC_ROUND_RNA)
+    return launch_split<tcec::kTF32, tcec::kRNA>(X, count, 0, hi, lo, d_flags, st);
+  if (rounding == TCEC_ROUND_RN)
+    return launch_split<tcec::kTF32, tcec::kRN>(X, count, 0, hi, lo, d_flags, st);
+  if (rounding == TCEC_ROUND_RZ)
+    return launch_split<tcec::kTF32, tcec::kRZ>(X, count, 0, hi, lo, d_flags, st);
+  return TCEC_ERR_UNSUPPORTED;
+}
+
+}  // extern "C"

@@ -1,0 +1,313 @@
+"""The drop-in GEMM entry point: gemm(a, b, scheme, cfg) -> GemmRun.
+
+Mirrors the reference's schemes.py (GemmKind :52-59, GemmScheme :62-84,
+factories :87-123, SCHEMES_BY_NAME :126-137, RunFlags / GemmRun :140-153,
+default_config :156-160, gemm :317-373) for the path this package accelerates:
+the three-term corrected scheme (`corrected3`) with the scaled FP16 split
+(FP16-TCEC) or the TF32 split (TF32-TCEC).  The compute runs in the sm_100a
+kernel behind include/tcec.h; there is no CPU fallback.  Other scheme kinds
+(the reference's CPU comparators and ablations) raise NotImplementedError.
+
+Error behaviour follows the reference: ValueError for non-2-D inputs,
+mismatched inner dimensions, non-finite inputs and non-FP32 values
+(schemes.py:163-171, :327-330); numerical anomalies only set RunFlags
+(schemes.py:237-241, :369-371).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import enum
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .formats import FP16, FP32, TF32, FloatFormat, RoundingMode
+from .splitting import (SplitScheme, markidis_halfhalf, native_split_args, scaled_halfhalf,
+                        tf32tf32)
+
+
+class GemmKind(enum.Enum):
+    FP64_REF = "fp64_ref"
+    FP32_SIMT = "fp32_simt"
+    FP32_LSBTRUNC = "fp32_lsbtrunc"
+    TC_PLAIN = "tc_plain"
+    MARKIDIS4 = "markidis4"
+    CORRECTED4 = "corrected4"
+    CORRECTED3 = "corrected3"
+
+
+@dataclass(frozen=True)
+class GemmScheme:
+    kind: GemmKind
+    split: SplitScheme | None = None
+    terminal: RoundingMode | None = None
+    conv_format: FloatFormat | None = None
+
+    @property
+    def label(self) -> str:
+        for name, scheme in SCHEMES_BY_NAME.items():
+            if scheme == self:
+                return name
+        return self.kind.value
+
+    @property
+    def input_format(self) -> FloatFormat | None:
+        if self.conv_format is not None:
+            return self.conv_format
+        if self.split is not None:
+            return self.split.low_format
+        return None
+
+
+def fp64_ref() -> GemmScheme:
+    return GemmScheme(GemmKind.FP64_REF)
+
+
+def fp32_simt() -> GemmScheme:
+    return GemmScheme(GemmKind.FP32_SIMT)
+
+
+def fp32_lsbtrunc() -> GemmScheme:
+    return GemmScheme(GemmKind.FP32_LSBTRUNC)
+
+
+def tc_plain(fmt: FloatFormat = FP16) -> GemmScheme:
+    return GemmScheme(GemmKind.TC_PLAIN, conv_format=fmt)
+
+
+def markidis4(fmt: FloatFormat = FP16) -> GemmScheme:
+    split = markidis_halfhalf() if fmt == FP16 else tf32tf32()
+    return GemmScheme(GemmKind.MARKIDIS4, split=split)
+
+
+def corrected4(terminal: RoundingMode, split: SplitScheme | None = None) -> GemmScheme:
+    if split is None:
+        split = markidis_halfhalf()
+    if split.scale_log2 != 0:
+        raise ValueError("corrected4 requires an unscaled split scheme")
+    return GemmScheme(GemmKind.CORRECTED4, split=split, terminal=terminal)
+
+
+def corrected3(split: SplitScheme | None = None) -> GemmScheme:
+    if split is None:
+        split = scaled_halfhalf()
+    return GemmScheme(GemmKind.CORRECTED3, split=split)
+
+
+SCHEMES_BY_NAME: dict[str, GemmScheme] = {
+    "fp64_ref": fp64_ref(),
+    "fp32_simt": fp32_simt(),
+    "fp32_lsbtrunc": fp32_lsbtrunc(),
+    "tc_plain_fp16": tc_plain(FP16),
+    "tc_plain_tf32": tc_plain(TF32),
+    "markidis4": markidis4(FP16),
+    "corrected4_rn": corrected4(RoundingMode.RN),
+    "corrected4_rz": corrected4(RoundingMode.RZ),
+    "corrected3_halfhalf": corrected3(scaled_halfhalf()),
+    "corrected3_tf32": corrected3(tf32tf32()),
+}
+
+
+@dataclass(frozen=True)
+class RunFlags:
+    saw_overflow: bool = False
+    saw_out_of_range: bool = False
+
+
+@dataclass(frozen=True)
+class GemmRun:
+    m: int
+    n: int
+    k: int
+    scheme: object
+    output: object
+    flags: RunFlags
+
+
+@dataclass(frozen=True)
+class MmaConfig:
+    """mma.py:26-45.  On the GPU, block_k is the drain interval of the main-term
+    partial (rounded up to a whole operand stage: 64 for FP16, 32 for TF32); the
+    accumulator width is the hardware's and acc_significand_bits is not used."""
+
+    input_format: FloatFormat = FP16
+    acc_significand_bits: int = 25
+    step_rounding: RoundingMode = RoundingMode.RZ
+    terminal_rounding: RoundingMode = RoundingMode.RZ
+    block_k: int = 16
+
+    def __post_init__(self) -> None:
+        if self.block_k < 1:
+            raise ValueError("block_k must be >= 1")
+        if not 1 <= self.acc_significand_bits <= 53:
+            raise ValueError("acc_significand_bits must be in [1, 53]")
+        if self.step_rounding is not RoundingMode.RZ:
+            raise ValueError("the emulated unit truncates between steps (RZ only)")
+
+
+def default_config(scheme, block_k: int = 16, acc_bits: int = 25) -> MmaConfig:
+    fmt = getattr(scheme, "input_format", None) or FP16
+    return MmaConfig(input_format=fmt, acc_significand_bits=acc_bits, block_k=block_k)
+
+
+STAGE_K = {N.TCEC_FP16: 64, N.TCEC_TF32: 32}
+
+
+def drain_k_for(variant: int, block_k: int) -> int:
+    """Drain interval the kernel uses for MmaConfig.block_k (whole operand stages)."""
+    stage = STAGE_K[variant]
+    return stage * max(1, -(-int(block_k) // stage))
+
+
+def resolve_scheme(scheme) -> tuple[int, int, int]:
+    """(variant, rounding code, scale_log2) for a corrected3 scheme.
+
+    Accepts a registry name, this package's GemmScheme, or the reference's
+    GemmScheme (duck-typed on .kind.value and .split).
+    """
+    if isinstance(scheme, str):
+        if scheme not in SCHEMES_BY_NAME:
+            raise ValueError(f"unknown scheme name: {scheme!r}")
+        scheme = SCHEMES_BY_NAME[scheme]
+    kind = getattr(getattr(scheme, "kind", None), "value", None)
+    if kind != GemmKind.CORRECTED3.value:
+        raise NotImplementedError(
+            f"scheme kind {kind!r} is a CPU comparator of the reference; only corrected3 "
+            "(FP16-TCEC / TF32-TCEC) runs on the sm_100a path")
+    return native_split_args(scheme.split)
+
+
+def _is_torch(x) -> bool:
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        return False
+    return isinstance(x, torch.Tensor)
+
+
+def _as_fp32_host(a) -> np.ndarray:
+    """schemes.py:163-171 for host inputs.  Finiteness is checked by the kernel
+    (its split warps raise TCEC_FLAG_NONFINITE_INPUT) so the host does not make
+    an extra pass over float32 data."""
+    x = np.asarray(a)
+    if x.ndim != 2:
+        raise ValueError("gemm expects 2-D matrices")
+    if x.dtype == np.float32:
+        return x
+    x64 = x.astype(np.float64)
+    if not np.all(np.isfinite(x64)):
+        raise ValueError("gemm requires finite inputs")
+    x32 = x64.astype(np.float32)
+    if not np.array_equal(x32.astype(np.float64), x64):
+        raise ValueError("inputs must hold FP32 values")
+    return x32
+
+
+def _flags_to_run(fl: int) -> RunFlags:
+    if fl & N.FLAG_NONFINITE_INPUT:
+        raise ValueError("gemm requires finite inputs")
+    return RunFlags(saw_overflow=bool(fl & N.FLAG_OVERFLOW),
+                    saw_out_of_range=bool(fl & N.FLAG_OUT_OF_RANGE))
+
+
+def _tma_ready(t):
+    """A CUDA fp32 tensor view with unit inner stride, a 16-byte aligned base and a
+    leading dimension that is a multiple of 4 floats (TMA); copies when needed."""
+    import torch
+
+    if t.stride(1) == 1 and t.stride(0) % 4 == 0 and t.stride(0) >= t.shape[1] \
+            and t.data_ptr() % 16 == 0:
+        return t, t.stride(0)
+    rows, cols = t.shape
+    ld = max(4, (cols + 3) // 4 * 4)
+    buf = torch.empty((rows, ld), dtype=torch.float32, device=t.device)
+    buf[:, :cols].copy_(t)
+    return buf[:, :cols], ld
+
+
+def gemm_device(a, b, scheme="corrected3_halfhalf", cfg: MmaConfig | None = None, out=None,
+                flags=None, block_n: int = 0, group_m: int = 0):
+    """C = A @ B on CUDA float32 tensors, stream-ordered on torch's current stream.
+
+    No host synchronisation: `flags` (int32 CUDA tensor, one element, caller
+    zeroed) receives the TCEC_FLAG_* bits.  Returns the output tensor.
+    """
+    import torch
+
+    variant, rounding, scale = resolve_scheme(scheme)
+    if a.dim() != 2 or b.dim() != 2:
+        raise ValueError("gemm expects 2-D matrices")
+    m, k = a.shape
+    kb, n = b.shape
+    if kb != k:
+        raise ValueError(f"inner dimensions differ: {k} vs {kb}")
+    if a.dtype != torch.float32 or b.dtype != torch.float32:
+        raise ValueError("inputs must hold FP32 values")
+    if not (a.is_cuda and b.is_cuda):
+        raise ValueError("gemm_device expects CUDA tensors")
+    if out is None:
+        ldc = max(4, (n + 3) // 4 * 4)
+        out = torch.empty((m, ldc), dtype=torch.float32, device=a.device)[:, :n]
+    if m == 0 or n == 0:
+        return out
+    if k == 0:  # zero blocks: C = 0 exactly (schemes.py:300-307)
+        return out.zero_()
+    block_k = cfg.block_k if cfg is not None else 16
+    opts = N.make_opts(split_rounding=rounding, scale_log2=scale,
+                       drain_k=drain_k_for(variant, block_k), block_n=block_n, group_m=group_m)
+    A, lda = _tma_ready(a)
+    B, ldb = _tma_ready(b)
+    C, ldc = out, out.stride(0)
+    if not (C.stride(1) == 1 and ldc % 4 == 0 and C.data_ptr() % 16 == 0):
+        raise ValueError("out must have unit inner stride and a 16-byte aligned leading dimension")
+    stream = torch.cuda.current_stream(a.device).cuda_stream
+    N.check(N.lib().tcec_sgemm(variant, m, n, k, A.data_ptr(), lda, B.data_ptr(), ldb,
+                               C.data_ptr(), ldc, ctypes.byref(opts),
+                               flags.data_ptr() if flags is not None else None, stream),
+            "tcec_sgemm")
+    return out
+
+
+def gemm(a, b, scheme, cfg: MmaConfig | None = None) -> GemmRun:
+    """schemes.py:317-373 for the corrected3 schemes, on the GPU.
+
+    numpy / array-like inputs: host buffers in, numpy float32 output (copies
+    through the C ABI's host entry, tcec_sgemm_host).  CUDA tensors: device
+    buffers, CUDA tensor output.  Either way the call synchronises once to read
+    the RunFlags, as the reference's GemmRun carries them.
+    """
+    variant, rounding, scale = resolve_scheme(scheme)
+    block_k = cfg.block_k if cfg is not None else 16
+    if _is_torch(a) and a.is_cuda:
+        import torch
+
+        if not (_is_torch(b) and b.is_cuda):
+            raise ValueError("both operands must live on the same kind of memory")
+        if a.dim() != 2 or b.dim() != 2:
+            raise ValueError("gemm expects 2-D matrices")
+        a32 = a if a.dtype == torch.float32 else a.to(torch.float32)
+        b32 = b if b.dtype == torch.float32 else b.to(torch.float32)
+        fl = torch.zeros(1, dtype=torch.int32, device=a.device)
+        out = gemm_device(a32, b32, scheme, cfg, flags=fl)
+        m, k = a.shape
+        n = b.shape[1]
+        return GemmRun(m=m, n=n, k=k, scheme=scheme, output=out,
+                       flags=_flags_to_run(int(fl.item())))
+    A = _as_fp32_host(a.cpu().numpy() if _is_torch(a) else a)
+    B = _as_fp32_host(b.cpu().numpy() if _is_torch(b) else b)
+    m, k = A.shape
+    kb, n = B.shape
+    if kb != k:
+        raise ValueError(f"inner dimensions differ: {k} vs {kb}")
+    A = np.ascontiguousarray(A)
+    B = np.ascontiguousarray(B)
+    C = np.empty((m, n), dtype=np.float32)
+    fl = ctypes.c_uint32(0)
+    opts = N.make_opts(split_rounding=rounding, scale_log2=scale,
+                       drain_k=drain_k_for(variant, block_k))
+    N.check(N.lib().tcec_sgemm_host(variant, m, n, k, A.ctypes.data, max(k, 1), B.ctypes.data,
+                                    max(n, 1), C.ctypes.data, max(n, 1), ctypes.byref(opts),
+                                    ctypes.byref(fl), None), "tcec_sgemm_host")
+    return GemmRun(m=m, n=n, k=k, scheme=scheme, output=C, flags=_flags_to_run(int(fl.value)))
