@@ -1,0 +1,375 @@
+"""Benchmark of the B200 error-corrected SGEMM (FP16-TCEC / TF32-TCEC).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--variant tf32|fp16] [--n 16384] [--allgather]
+
+One step = one error-corrected GEMM of the workload (default: TF32-TCEC,
+m = n = k = 16384, BASELINE.json configs[1] at the size its metric is quoted
+on).  Inputs are 1 GiB FP32 matrices each (> the 126 MB L2), so no L2 flush is
+needed between steps.  Under torchrun (N > 1) every rank computes its own
+16384-row slab of an (N*16384) x 16384 x 16384 product with B replicated
+(weak scaling, no data-path collective; --allgather adds the optional NCCL
+all-gather of C inside the timed region).
+
+Rank 0 prints one JSON line.  `value` is whole-job effective TFLOP/s
+(2*m*n*k / max-over-ranks time); `e2e` is the same metric through the public
+API with host buffers (pinned H2D of A and B and D2H of C inside the timed
+region); `roofline` relates the GEMM kernel to the 3-product tensor roofline;
+`cpu_baseline` times the CPU oracle (a restatement of the reference's
+algorithm) on a bounded sub-block on this host.
+
+--impl reference times the reference's CPU algorithm (the C oracle port, all
+host threads) on a bounded sample of the same workload and prints the same
+metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary.json")
+
+METRIC = "effective FP32 TFLOP/s at n=16384 vs FP32 SIMT peak; rel. error vs FP64 = SGEMM"
+SCHEME = {"tf32": "corrected3_tf32", "fp16": "corrected3_halfhalf"}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--variant", choices=["tf32", "fp16"], default="tf32")
+    p.add_argument("--n", type=int, default=16384)
+    p.add_argument("--allgather", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-extras", action="store_true", help="skip cuBLAS / accuracy / other variant")
+    p.add_argument("--cpu-sample-seconds", type=float, default=15.0)
+    return p.parse_args()
+
+
+def load_peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "sm_max_mhz": 1965.0}, "fallback"
+
+
+# ----------------------------------------------------------------- clocks ---
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, mx, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+                power.append(float(parts[3]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "samples": len(sm),
+                "power_w_max": max(power) if power else None, "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------ CPU oracle ---
+def cpu_oracle_sample(variant: str, k: int, seconds: float, threads: int):
+    """Time the CPU oracle (test-infrastructure restatement of the reference's
+    corrected3 path, oracle/tcec_oracle.c) on a sub-block rows x cols x k of
+    the workload, sized to take about `seconds` on `threads` host threads."""
+    from oracle import oracle as O
+
+    bk = 16 if variant == "fp16" else 8
+    # calibrate on threads x 8 outputs, then size a threads*R x 64 block
+    a = O.urand(threads, k, -1, 1, 11)
+    b = O.urand(k, 8, -1, 1, O.pair_seed(11))
+    t0 = time.perf_counter()
+    O.corrected3(a, b, variant, block_k=bk, nthreads=threads)
+    t_small = max(time.perf_counter() - t0, 1e-4)
+    cols = 64
+    reps = max(1, int(round(seconds / (t_small * cols / 8))))
+    rows = min(threads * reps, 8192)
+    a = O.urand(rows, k, -1, 1, 12)
+    b = O.urand(k, cols, -1, 1, O.pair_seed(12))
+    t0 = time.perf_counter()
+    O.corrected3(a, b, variant, block_k=bk, nthreads=threads)
+    dt = time.perf_counter() - t0
+    flops = 2.0 * rows * cols * k
+    return {"value": flops / dt / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "port",
+            "sample": f"oracle corrected3 ({variant}) on a {rows}x{cols} output block at k={k} "
+                      f"({dt:.1f} s); full reference algorithm per output",
+            "seconds": dt}
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm (C oracle port) on host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    vals = []
+    sample = None
+    steps_s = max(1.0, 60.0 / max(1, args.steps + args.warmup))
+    for i in range(args.warmup + args.steps):
+        r = cpu_oracle_sample(args.variant, args.n, steps_s, threads)
+        if i >= args.warmup:
+            vals.append(r["value"])
+            sample = r
+    v = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sample["seconds"] * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic urand(-1,1)",
+        "config": {"workload": f"{'TF32' if args.variant == 'tf32' else 'FP16'}-TCEC SGEMM "
+                               f"m=n=k={args.n} (bounded output sub-block on host cores)",
+                   "variant": args.variant, "m": args.n, "n": args.n, "k": args.n},
+        "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": threads, "kind": "port",
+                         "sample": sample["sample"]},
+        "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ ours ---
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2203_03341_b200 as T
+    from paper_2203_03341_b200 import _native as Nat
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cudnn.allow_tf32 = False
+    torch.set_float32_matmul_precision("highest")
+
+    n = args.n
+    scheme = SCHEME[args.variant]
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    A = (torch.rand((n, n), generator=gen, device=dev) * 2 - 1).contiguous()
+    gen.manual_seed(99)  # B replicated: identical on every rank
+    B = (torch.rand((n, n), generator=gen, device=dev) * 2 - 1).contiguous()
+    C = torch.empty((n, n), device=dev)
+    Cfull = torch.empty((n * world, n), device=dev) if (args.allgather and world > 1) else None
+    stream = torch.cuda.current_stream(dev)
+    flops_step = 2.0 * n * n * n  # per rank
+
+    def step():
+        T.gemm_device(A, B, scheme, out=C)
+        if Cfull is not None:
+            dist.all_gather_into_tensor(Cfull, C)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    launches0 = Nat.launch_count()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    launches = Nat.launch_count() - launches0
+    ms = ev0.elapsed_time(ev1) / args.steps
+    t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * flops_step / (ms_max * 1e-3) / 1e12
+
+    peaks, peak_basis = load_peaks()
+    bf16 = float(peaks.get("bf16_tflops", 1590.0))
+    dense = bf16 if args.variant == "fp16" else bf16 / 2.0
+    kernel_ms = ms  # one launch per step (the all-gather is not the dominant kernel)
+    eff = flops_step / (kernel_ms * 1e-3) / 1e12
+    traffic = None
+    try:
+        with open(NCU_SUMMARY) as f:
+            summ = json.load(f)
+        entry = summ.get(f"{args.variant}_{n}")
+        if entry:
+            traffic = entry.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    roofline = {"bound": "tensor", "achieved": eff, "peak": dense / 3.0, "unit": "TFLOP/s",
+                "frac": eff / (dense / 3.0), "traffic": traffic,
+                "peak_basis": f"{'FP16' if args.variant == 'fp16' else 'TF32'} dense / 3 products; "
+                              f"dense = {peak_basis} bf16 burst {bf16:.1f} TF/s"
+                              + ("" if args.variant == "fp16" else " / 2 (TF32 rate)"),
+                "algorithmic_flops_per_launch": flops_step,
+                "algorithmic_bytes_per_launch": 4.0 * 3 * n * n}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic urand(-1,1) FP32 (torch Philox on device)",
+        "config": {"workload": f"{'TF32' if args.variant == 'tf32' else 'FP16'}-TCEC SGEMM "
+                               f"m=n=k={n} per rank" + (", row-sharded" if world > 1 else ""),
+                   "variant": args.variant, "scheme": scheme, "m": n * world, "n": n, "k": n,
+                   "parallelism": f"row-shard x{world}" + (" + all-gather C" if Cfull is not None else ""),
+                   "l2": "inputs 1 GiB each > 126 MB L2 (no flush needed)"},
+        "clocks": clk, "gpu_launches": int(launches),
+        "roofline": roofline,
+    }
+    if rank == 0:
+        fp32_simt_peak = 148 * 128 * 2 * (clk.get("sm_max_mhz") or 1965.0) * 1e6 / 1e12
+        line["fp32_simt_peak_tflops"] = fp32_simt_peak
+        line["vs_fp32_simt_peak"] = (value / world) / fp32_simt_peak
+
+    # -------- extras on rank 0: cuBLAS SGEMM, accuracy vs FP64, other variant
+    if rank == 0 and not args.no_extras:
+        extras = {}
+        # cuBLAS SGEMM (SIMT: TF32 off) at the same size
+        for _ in range(2):
+            torch.matmul(A, B, out=C)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        reps = 3
+        e0.record(stream)
+        for _ in range(reps):
+            torch.matmul(A, B, out=C)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        extras["cublas_sgemm_tflops"] = flops_step / (e0.elapsed_time(e1) / reps * 1e-3) / 1e12
+        # accuracy vs FP64 on a 256-row sub-block (relative residual, Eq. 7)
+        rows = slice(0, 256)
+        ref = torch.matmul(A[rows].double(), B.double())
+        acc = {}
+        for v in ("tf32", "fp16"):
+            Cv = T.gemm_device(A, B, SCHEME[v])
+            acc[f"relres_{v}_tcec"] = float(torch.linalg.norm(ref - Cv[rows].double()) / torch.linalg.norm(ref))
+        Cs = torch.matmul(A[rows], B)
+        acc["relres_cublas_sgemm"] = float(torch.linalg.norm(ref - Cs.double()) / torch.linalg.norm(ref))
+        extras["accuracy_vs_fp64_256rows"] = acc
+        # the other variant's throughput (same procedure)
+        other = "fp16" if args.variant == "tf32" else "tf32"
+        for _ in range(2):
+            T.gemm_device(A, B, SCHEME[other], out=C)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(max(3, args.steps // 2)):
+            T.gemm_device(A, B, SCHEME[other], out=C)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms_o = e0.elapsed_time(e1) / max(3, args.steps // 2)
+        extras[f"{other}_tcec_tflops"] = flops_step / (ms_o * 1e-3) / 1e12
+        line["extras"] = extras
+        del Cs, ref
+
+    # -------- e2e through the public API with host buffers (pinned)
+    if not args.no_e2e:
+        del C
+        torch.cuda.empty_cache()
+        hA = torch.empty((n, n), dtype=torch.float32, pin_memory=True)
+        hB = torch.empty((n, n), dtype=torch.float32, pin_memory=True)
+        hA.copy_(A)
+        hB.copy_(B)
+        del A, B
+        torch.cuda.empty_cache()
+        npA, npB = hA.numpy(), hB.numpy()
+        e2e_steps = max(2, min(args.steps, 5))
+        T.gemm(npA, npB, scheme)  # warm-up (pool, descriptors)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            run = T.gemm(npA, npB, scheme)  # H2D A,B -> kernel -> D2H C, sync
+        torch.cuda.synchronize()
+        dt = (time.perf_counter() - t0) / e2e_steps
+        tt = torch.tensor([dt], device=dev)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dt = float(tt.item())
+        line["e2e"] = {"value": world * flops_step / dt / 1e12, "unit": "TFLOP/s",
+                       "h2d_bytes_per_step": 2 * n * n * 4, "d2h_bytes_per_step": n * n * 4,
+                       "ms_per_step": dt * 1e3,
+                       "path": "paper_2203_03341_b200.gemm(numpy pinned) -> tcec_sgemm_host"}
+        del run
+
+    if rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_oracle_sample(args.variant, n, args.cpu_sample_seconds,
+                                                 os.cpu_count() or 1)
+        line["cpu_baseline"].pop("seconds", None)
+
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

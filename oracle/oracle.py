@@ -31,6 +31,7 @@ FLAG_OVERFLOW, FLAG_OUT_OF_RANGE = 1, 2
 VARIANTS = {
     "fp16": (FMT_FP16, 11, RM_RN),
     "tf32": (FMT_TF32, 0, RM_RNA),
+    "fp16u": (FMT_FP16, 0, RM_RN),  # markidis_halfhalf (splitting.py:70-71), unscaled
 }
 
 

@@ -121,6 +121,12 @@ int resolve_rounding(int variant, int rounding) {
   return rounding;
 }
 
+// Built (variant, rounding) pairs: FP16 {RN, RZ} (cvt.rn / cvt.rz), TF32 {RN, RNA, RZ}.
+bool rounding_supported(int variant, int rounding) {
+  if (variant == TCEC_FP16) return rounding == TCEC_ROUND_RN || rounding == TCEC_ROUND_RZ;
+  return rounding == TCEC_ROUND_RN || rounding == TCEC_ROUND_RNA || rounding == TCEC_ROUND_RZ;
+}
+
 template <int V, int R>
 int launch_split(const float* X, int64_t count, int scale_log2, float* hi, float* lo,
                  uint32_t* d_flags, cudaStream_t stream) {
@@ -173,6 +179,7 @@ int tcec_sgemm(int variant, int64_t m, int64_t n, int64_t k, const float* A, int
   o.scale_log2 = -1;
   if (opts) o = *opts;
   const int rounding = resolve_rounding(variant, o.split_rounding);
+  if (!rounding_supported(variant, rounding)) return TCEC_ERR_UNSUPPORTED;
   int scale_log2 = o.scale_log2 < 0 ? (variant == TCEC_FP16 ? 11 : 0) : o.scale_log2;
   if (variant == TCEC_TF32 && scale_log2 != 0) return TCEC_ERR_UNSUPPORTED;
   if (variant == TCEC_FP16 && scale_log2 != 0 && scale_log2 != 11) return TCEC_ERR_UNSUPPORTED;
@@ -183,6 +190,7 @@ int tcec_sgemm(int variant, int64_t m, int64_t n, int64_t k, const float* A, int
     drain_every = o.drain_k / bk_op;
   }
   const int block_n = o.block_n == 0 ? 128 : o.block_n;
+  if (block_n != 128) return TCEC_ERR_UNSUPPORTED;
   const int group_m = o.group_m <= 0 ? 16 : o.group_m;
   if (m == 0 || n == 0) return TCEC_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -276,6 +284,7 @@ int tcec_split(int variant, int rounding, int scale_log2, const float* X, int64_
   if (count < 0) return TCEC_ERR_ARG;
   if (count == 0) return TCEC_OK;
   rounding = resolve_rounding(variant, rounding);
+  if (!rounding_supported(variant, rounding)) return TCEC_ERR_UNSUPPORTED;
   if (scale_log2 < 0) scale_log2 = variant == TCEC_FP16 ? 11 : 0;
   if (variant == TCEC_TF32 && scale_log2 != 0) return TCEC_ERR_UNSUPPORTED;
   if (variant == TCEC_FP16 && scale_log2 != 0 && scale_log2 != 11) return TCEC_ERR_UNSUPPORTED;

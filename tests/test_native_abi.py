@@ -1,0 +1,88 @@
+"""CPU checks of the C ABI boundary: the library builds, loads, exports every
+symbol include/tcec.h declares, and rejects bad arguments before touching the
+GPU.  No compute calls are made here."""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2203_03341_b200 import _native as N
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "tcec.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    N.build()
+    return N.lib()
+
+
+def _declared_functions():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?\w+\s*\**\s*(tcec_\w+)\s*\(", text, flags=re.M)))
+
+
+def test_header_declares_expected_entry_points():
+    assert _declared_functions() == sorted(N.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol(lib):
+    for name in _declared_functions():
+        assert hasattr(lib, name), name
+        assert ctypes.cast(getattr(lib, name), ctypes.c_void_p).value
+
+
+def test_version_and_status_strings(lib):
+    assert lib.tcec_version() == 100
+    for code in (N.OK, N.ERR_ARG, N.ERR_ALIGN, N.ERR_UNSUPPORTED, N.ERR_CUDA, N.ERR_ARCH):
+        assert lib.tcec_status_str(code).decode()
+    assert lib.tcec_status_str(12345).decode() == "unknown status"
+
+
+def test_opts_struct_matches_header():
+    # int32 x 5 + int32[3]
+    assert ctypes.sizeof(N.TcecOpts) == 32
+
+
+def test_argument_validation_without_gpu(lib):
+    f = lib.tcec_sgemm
+    # unknown variant / negative sizes / short leading dimensions: rejected before any CUDA call
+    assert f(7, 4, 4, 4, None, 4, None, 4, None, 4, None, None, None) == N.ERR_ARG
+    assert f(0, -1, 4, 4, None, 4, None, 4, None, 4, None, None, None) == N.ERR_ARG
+    assert f(0, 4, 4, 8, None, 4, None, 4, None, 4, None, None, None) == N.ERR_ARG
+    assert f(0, 4, 8, 4, None, 4, None, 4, None, 4, None, None, None) == N.ERR_ARG
+    # empty output: no-op success
+    assert f(0, 0, 4, 4, None, 4, None, 4, None, 4, None, None, None) == N.OK
+    assert f(1, 4, 0, 4, None, 4, None, 4, None, 4, None, None, None) == N.OK
+    # unsupported option combinations
+    o = N.make_opts(split_rounding=N.ROUND_RN, scale_log2=5)
+    assert f(0, 4, 4, 4, None, 4, None, 4, None, 4, ctypes.byref(o), None, None) == N.ERR_UNSUPPORTED
+    o = N.make_opts(drain_k=48)
+    assert f(0, 4, 4, 4, None, 4, None, 4, None, 4, ctypes.byref(o), None, None) == N.ERR_UNSUPPORTED
+    o = N.make_opts(scale_log2=11)
+    assert f(1, 4, 4, 4, None, 4, None, 4, None, 4, ctypes.byref(o), None, None) == N.ERR_UNSUPPORTED
+    s = lib.tcec_split
+    assert s(3, -1, -1, None, 4, None, None, None, None) == N.ERR_ARG
+    assert s(0, -1, -1, None, -4, None, None, None, None) == N.ERR_ARG
+    assert s(0, -1, -1, None, 0, None, None, None, None) == N.OK
+    assert s(0, N.ROUND_RNA, -1, None, 4, None, None, None, None) == N.ERR_UNSUPPORTED
+
+
+def test_sass_contains_tcgen05_and_tma():
+    """The built library carries tcgen05 MMA (UTC*MMA), TMEM loads (LDTM) and
+    TMA (UTMALDG/UTMASTG) -- the Blackwell-native path, not legacy HMMA."""
+    import shutil
+    import subprocess
+
+    if shutil.which("cuobjdump") is None:
+        pytest.skip("cuobjdump not available")
+    N.build()
+    out = subprocess.run(["cuobjdump", "-sass", N.LIB_PATH], capture_output=True, text=True,
+                         check=True).stdout
+    for mnem in ("UTCHMMA", "LDTM", "UTMALDG", "UTMASTG"):
+        assert mnem in out, mnem
+    assert re.search(r"\bHMMA\b", out) is None
