@@ -53,7 +53,7 @@ typedef struct tcec_opts {
    * mma.py:34): 0 = one operand stage (64 for FP16, 32 for TF32); otherwise a
    * positive multiple of that stage depth. */
   int32_t drain_k;
-  /* Output tile width: 0 = default (128). */
+  /* Output tile width: 0 = default (256: CTA-pair 256 x 256 tile); 128 = single-CTA 128 x 128. */
   int32_t block_n;
   /* Tile rasterisation group along m: 0 = default (16). */
   int32_t group_m;

@@ -189,5 +189,148 @@ __host__ __device__ constexpr uint32_t umma_idesc(uint32_t ab_format, uint32_t M
          | ((M >> 4) << 24);       // m_dim
 }
 
+
+// ----------------------------------------------------------------- clusters --
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n"
+               "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// shared::cta address of this CTA -> shared::cluster address of the same
+// offset in CTA `rank` of the cluster.
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+
+// Arrive on an mbarrier in another CTA of the cluster (release at cluster scope).
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+
+// Wait with acquire at cluster scope (for barriers that peer CTAs arrive on).
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITC_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAITC_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+
+// ---------------------------------------------------------- tcgen05 (pair) --
+template <uint32_t kCols>
+__device__ __forceinline__ void tmem_alloc_pair(uint32_t* dst_smem) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   smem_u32(dst_smem)),
+               "n"(kCols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+
+template <uint32_t kCols>
+__device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols)
+               : "memory");
+}
+
+// CTA-pair MMA (M = 256 across the pair), issued by the leader CTA only.
+template <bool kTF32>
+__device__ __forceinline__ void mma_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t idesc, uint32_t accumulate) {
+  if constexpr (kTF32) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+  }
+}
+
+// Arrive on the mbarrier at this offset in every CTA of `cta_mask` once all
+// prior tcgen05 ops of the pair have completed.
+__device__ __forceinline__ void mma_commit_pair_mc(uint64_t* bar, uint16_t cta_mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(cta_mask)
+      : "memory");
+}
+
+// Register-count hand-off between warpgroups (all 4 warps of a group execute it).
+template <uint32_t kRegs>
+__device__ __forceinline__ void regs_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegs));
+}
+template <uint32_t kRegs>
+__device__ __forceinline__ void regs_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegs));
+}
+
+// MN-major swizzled operand descriptor: atoms of 128-byte MN rows (8 rows for
+// SWIZZLE_128B, layout 2; 4 rows for SWIZZLE_128B_BASE32B, layout 1 -- the only
+// MN-major layout for 32-bit TF32 operands); LBO = byte stride between MN
+// atoms, SBO = byte stride between K row-groups.
+__device__ __forceinline__ uint64_t umma_desc_mnmajor(uint32_t smem_addr, uint32_t lbo,
+                                                      uint32_t sbo, uint32_t layout) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((smem_addr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+  d |= static_cast<uint64_t>(1u) << 46;
+  d |= static_cast<uint64_t>(layout & 7u) << 61;
+  return d;
+}
+
+// Instruction descriptor with an MN-major B operand (bit 16).
+__host__ __device__ constexpr uint32_t umma_idesc_bmn(uint32_t ab_format, uint32_t M, uint32_t N) {
+  return umma_idesc(ab_format, M, N) | (1u << 16);
+}
+
+// ------------------------------------------------------------- packed FP32 --
+// (x0, x1) * s and fma((h0, h1), t, (y0, y1)) on the sm_100 f32x2 pipe.
+__device__ __forceinline__ void residual_x2(float x0, float x1, float h0, float h1, float s,
+                                            float& r0, float& r1) {
+  // r = (x - h) * s computed as fma(h, -s, x * s): both products are exact
+  // (power-of-two s, no overflow while h is finite) and the fma rounds the
+  // exact, representable difference once -- bit-identical to (x - h) * s.
+  asm("{\n"
+      ".reg .b64 xv, hv, sv, nv, rv;\n"
+      "mov.b64 xv, {%2, %3};\n"
+      "mov.b64 hv, {%4, %5};\n"
+      "mov.b64 sv, {%6, %6};\n"
+      "mov.b64 nv, {%7, %7};\n"
+      "mul.rn.f32x2 xv, xv, sv;\n"
+      "fma.rn.f32x2 rv, hv, nv, xv;\n"
+      "mov.b64 {%0, %1}, rv;\n"
+      "}\n"
+      : "=f"(r0), "=f"(r1)
+      : "f"(x0), "f"(x1), "f"(h0), "f"(h1), "f"(s), "f"(-s));
+}
+
 }  // namespace sm100
 }  // namespace tcec

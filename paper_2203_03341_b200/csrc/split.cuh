@@ -29,12 +29,13 @@ constexpr uint32_t kFlagNonfiniteInput = 4u;
 
 // ------------------------------------------------------------------ FP16 --
 // cvt.{rn,rz}.f16x2.f32: IEEE conversion with gradual underflow; RN overflows
-// to inf (formats.py:140), RZ saturates to 65504 (formats.py:137-138).
+// to inf (formats.py:140); RZ saturates to 65504 (formats.py:137-138), which
+// needs .satfinite (plain cvt.rz returns inf for inputs near FLT_MAX).
 template <int R>
 __device__ __forceinline__ uint32_t cvt_f16x2(float lo_elem, float hi_elem) {
   uint32_t d;
   if constexpr (R == kRZ) {
-    asm("cvt.rz.f16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi_elem), "f"(lo_elem));
+    asm("cvt.rz.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi_elem), "f"(lo_elem));
   } else {
     asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi_elem), "f"(lo_elem));
   }

@@ -15,6 +15,7 @@
 
 #include "tcec.h"
 #include "tcec_gemm.cuh"
+#include "tcec_gemm2.cuh"
 
 namespace {
 
@@ -105,10 +106,52 @@ int launch_gemm(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, co
 }
 
 template <int V, int R>
+int launch_gemm_pair(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, const float* B,
+                     int64_t ldb, float* C, int64_t ldc, int scale_log2, int drain_every,
+                     int group_m, uint32_t* d_flags, cudaStream_t stream) {
+  using Cfg = tcec::PairCfg<V>;
+  using VC = tcec::VarCfg<V>;
+  CUtensorMap tmA, tmB, tmC;
+  int st;
+  if ((st = make_tmap(&tmA, A, k, m, lda, Cfg::BK_STG, Cfg::BM, CU_TENSOR_MAP_SWIZZLE_128B)))
+    return st;
+  if ((st = make_tmap(&tmB, B, n, k, ldb, 32, Cfg::BK_STG, CU_TENSOR_MAP_SWIZZLE_128B))) return st;
+  if ((st = make_tmap(&tmC, C, n, m, ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B))) return st;
+
+  auto kern = tcec::tcec_gemm_pair_kernel<V, R>;
+  static std::once_flag attr_once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(attr_once, [&] {
+    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    Cfg::SMEM_BYTES);
+  });
+  if (attr_err != cudaSuccess) return TCEC_ERR_CUDA;
+
+  tcec::GemmShape shp;
+  shp.m = static_cast<int32_t>(m);
+  shp.n = static_cast<int32_t>(n);
+  shp.k = static_cast<int32_t>(k);
+  shp.num_op_stages = static_cast<int32_t>((k + VC::BK_OP - 1) / VC::BK_OP);
+  shp.drain_every = drain_every;
+  shp.group_m = group_m;
+  const float scale = ldexpf(1.0f, scale_log2);
+  const float inv_scale = ldexpf(1.0f, -scale_log2);
+  const tcec::FlagThresholds thr = tcec::flag_thresholds(V, R, scale_log2);
+  const int64_t pairs = ((m + 2 * Cfg::BM - 1) / (2 * Cfg::BM)) * ((n + Cfg::BN - 1) / Cfg::BN);
+  kern<<<static_cast<unsigned>(2 * pairs), Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream>>>(
+      tmA, tmB, tmC, shp, scale, inv_scale, thr, d_flags);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError() == cudaSuccess ? TCEC_OK : TCEC_ERR_CUDA;
+}
+
+template <int V, int R>
 int dispatch_bn(int bn, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda,
                 const float* B, int64_t ldb, float* C, int64_t ldc, int s, int de, int gm,
                 uint32_t* fl, cudaStream_t st) {
   switch (bn) {
+    case 256:
+      return launch_gemm_pair<V, R>(m, n, k, A, lda, B, ldb, C, ldc, s, de, gm / 2 > 0 ? gm / 2 : 1,
+                                    fl, st);
     case 128:
       return launch_gemm<V, R, 128>(m, n, k, A, lda, B, ldb, C, ldc, s, de, gm, fl, st);
     default:
@@ -189,8 +232,8 @@ int tcec_sgemm(int variant, int64_t m, int64_t n, int64_t k, const float* A, int
     if (o.drain_k < 0 || o.drain_k % bk_op != 0) return TCEC_ERR_UNSUPPORTED;
     drain_every = o.drain_k / bk_op;
   }
-  const int block_n = o.block_n == 0 ? 128 : o.block_n;
-  if (block_n != 128) return TCEC_ERR_UNSUPPORTED;
+  const int block_n = o.block_n == 0 ? 256 : o.block_n;
+  if (block_n != 128 && block_n != 256) return TCEC_ERR_UNSUPPORTED;
   const int group_m = o.group_m <= 0 ? 16 : o.group_m;
   if (m == 0 || n == 0) return TCEC_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);

@@ -1,0 +1,425 @@
+// tcec_gemm2.cuh -- CTA-pair (cta_group::2) fused error-corrected SGEMM.
+//
+// Same algorithm as tcec_gemm.cuh (the reference's corrected3 path,
+// schemes.py:265-314) on a 256 x 256 output tile shared by a cluster of two
+// CTAs on one TPC.  Each CTA stages and splits its own 128 rows of A and its
+// own 128 columns of B; the leader CTA issues tcgen05.mma.cta_group::2 with
+// M = 256, N = 256, which reads A from each CTA's shared memory and B from both
+// halves; each CTA's TMEM receives its 128 rows.  Per SM this halves the
+// split work and the tensor-core operand traffic per flop relative to the
+// single-CTA 128 x 128 tile.
+//
+// Warp roles (640 threads, 20 warps, one CTA per SM):
+//   warp 0        TMA producer: FP32 A [128 x 32] and B [32 x 128] k-slices
+//   warp 1        MMA issuer (leader CTA only)
+//   warp 2        TMEM allocator (512 columns: P | dC)
+//   warps 4-11    split: FP32 slice -> (hi, lo) operands.  A is stored K-major,
+//                 B MN-major (no transpose), both 128-byte swizzled.
+//   warps 12-19   drain: C = RN32(C + P) per operand stage (C in registers),
+//                 epilogue C = RN32(C + dC * 2^-s) -> TMA store.
+#pragma once
+
+#include "tcec_gemm.cuh"
+
+namespace tcec {
+
+template <int V>
+struct PairCfg {
+  static constexpr int BM = 128;           // rows per CTA (pair M = 256)
+  static constexpr int BN = 256;           // pair N = MMA N
+  static constexpr int BN_CTA = 128;       // B columns staged / split per CTA
+  static constexpr int BK_STG = 32;        // FP32 k per staging slice
+  static constexpr int NSTG = 3;
+  static constexpr int NOP = 2;
+  static constexpr int STG_A_BYTES = BM * BK_STG * 4;      // 16 KB, SW128 rows of 32 k
+  static constexpr int STG_B_BOX = BK_STG * 32 * 4;        // 4 KB box: 32 k x 32 n, SW128
+  static constexpr int STG_B_BYTES = 4 * STG_B_BOX;        // 16 KB
+  static constexpr int STG_BYTES = STG_A_BYTES + STG_B_BYTES;
+  static constexpr int OP_A_BYTES = BM * 128;              // K-major, 128-byte k rows
+  static constexpr int OP_B_BYTES = BN_CTA * VarCfg<V>::BK_OP * (V == kFP16 ? 2 : 4);  // 16 KB
+  static constexpr int OP_BYTES = 2 * OP_A_BYTES + 2 * OP_B_BYTES;
+  // MN-major B: atoms of 128-byte n-rows, B_ROWS k-rows each (FP16: SWIZZLE_128B,
+  // 64 n x 8 k; TF32: SWIZZLE_128B_BASE32B, 32 n x 4 k); atoms along n, then
+  // k-groups.
+  static constexpr int B_ATOM_N = V == kFP16 ? 64 : 32;     // n per 128-byte row
+  static constexpr int B_ROWS = V == kFP16 ? 8 : 4;         // k rows per atom
+  static constexpr int B_LBO = B_ROWS * 128;                // next atom along n
+  static constexpr int B_SBO = (BN_CTA / B_ATOM_N) * B_LBO; // next k-group
+  static constexpr uint32_t B_LAYOUT = V == kFP16 ? 2u : 1u;
+  static constexpr int B_KSTEP_BYTES = (V == kFP16 ? 16 : 8) / B_ROWS * B_SBO;  // per MMA k-step
+  static constexpr int OFF_STG = 0;
+  static constexpr int OFF_OP = NSTG * STG_BYTES;
+  static constexpr int OFF_BAR = OFF_OP + NOP * OP_BYTES;
+  static constexpr int NUM_BARS = 2 * NSTG + 2 * NOP + 2;
+  static constexpr int SMEM_BYTES = OFF_BAR + NUM_BARS * 8 + 16 + 1024;
+  static constexpr int TMEM_COLS = 512;                    // P [0,256) | dC [256,512)
+  static constexpr int NUM_THREADS = 640;
+  static constexpr int SPLIT_WARP0 = 4, NUM_SPLIT_WARPS = 8;
+  static constexpr int DRAIN_WARP0 = 12, NUM_DRAIN_WARPS = 8;
+  static constexpr int EPI_WARP_BYTES = 32 * 128 * 4;      // 32 rows x 128 cols per drain warp
+  static_assert(B_KSTEP_BYTES == 4096, "B advance per k-step");
+  static_assert(OP_B_BYTES == 16384, "B operand stage size");
+  static_assert(NUM_DRAIN_WARPS * EPI_WARP_BYTES <= OFF_BAR, "epilogue staging reuses the rings");
+};
+
+// Split one 32-deep FP32 slice of this CTA's A rows and B columns into the
+// operand stage.  Thread t (0..255):
+//   A: row r = t & 127, k in [16 (t >> 7), +16)        -> K-major hi / lo
+//   B: k = t & 31, n in [16 (t >> 5), +16)             -> MN-major hi / lo
+// With kFlags the thread also folds its inputs into the RunFlags accumulator
+// (only the CTAs designated to cover each element of A / B exactly once).
+template <int V, int R, bool kFlags>
+__device__ __forceinline__ void pair_split_slice(const uint8_t* stg, uint8_t* op, int sub, int t,
+                                                 float scale, FlagAcc& fa) {
+  using C = PairCfg<V>;
+  uint8_t* opAhi = op;
+  uint8_t* opAlo = op + C::OP_A_BYTES;
+  uint8_t* opBhi = op + 2 * C::OP_A_BYTES;
+  uint8_t* opBlo = opBhi + C::OP_B_BYTES;
+
+  // ------------------------------------------------------------------ A
+  {
+    const int r = t & 127;
+    const int half = t >> 7;
+    float x[16];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float4 v = *reinterpret_cast<const float4*>(stg + sw128(r, half * 4 + i));
+      x[4 * i] = v.x;
+      x[4 * i + 1] = v.y;
+      x[4 * i + 2] = v.z;
+      x[4 * i + 3] = v.w;
+    }
+    if constexpr (kFlags) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) fa.add(x[i]);
+    }
+    if constexpr (V == kFP16) {
+      uint32_t hp[8], lp[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        hp[j] = cvt_f16x2<R>(x[2 * j], x[2 * j + 1]);
+        float h0, h1, r0, r1;
+        unpack_f16x2(hp[j], h0, h1);
+        sm100::residual_x2(x[2 * j], x[2 * j + 1], h0, h1, scale, r0, r1);
+        lp[j] = cvt_f16x2<R>(r0, r1);
+      }
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const uint32_t off = sw128(r, sub * 4 + half * 2 + q);
+        *reinterpret_cast<uint4*>(opAhi + off) = make_uint4(hp[4 * q], hp[4 * q + 1], hp[4 * q + 2], hp[4 * q + 3]);
+        *reinterpret_cast<uint4*>(opAlo + off) = make_uint4(lp[4 * q], lp[4 * q + 1], lp[4 * q + 2], lp[4 * q + 3]);
+      }
+    } else {
+      float hf[16], lf[16];
+#pragma unroll
+      for (int j = 0; j < 16; j += 2) {
+        hf[j] = __uint_as_float(tf32_round_bits<R>(__float_as_uint(x[j])));
+        hf[j + 1] = __uint_as_float(tf32_round_bits<R>(__float_as_uint(x[j + 1])));
+        float r0, r1;
+        sm100::residual_x2(x[j], x[j + 1], hf[j], hf[j + 1], 1.0f, r0, r1);
+        lf[j] = __uint_as_float(tf32_round_bits<R>(__float_as_uint(r0)));
+        lf[j + 1] = __uint_as_float(tf32_round_bits<R>(__float_as_uint(r1)));
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t off = sw128(r, half * 4 + q);
+        *reinterpret_cast<float4*>(opAhi + off) = make_float4(hf[4 * q], hf[4 * q + 1], hf[4 * q + 2], hf[4 * q + 3]);
+        *reinterpret_cast<float4*>(opAlo + off) = make_float4(lf[4 * q], lf[4 * q + 1], lf[4 * q + 2], lf[4 * q + 3]);
+      }
+    }
+  }
+  // ------------------------------------------------------------------ B
+  {
+    const int k = t & 31;
+    const int qn = t >> 5;                 // 16-column group
+    const uint8_t* box = stg + C::STG_A_BYTES + (qn >> 1) * C::STG_B_BOX;
+    float x[16];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float4 v = *reinterpret_cast<const float4*>(box + sw128(k, (qn & 1) * 4 + i));
+      x[4 * i] = v.x;
+      x[4 * i + 1] = v.y;
+      x[4 * i + 2] = v.z;
+      x[4 * i + 3] = v.w;
+    }
+    if constexpr (kFlags) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) fa.add(x[i]);
+    }
+    const int kop = sub * 32 + k;          // k within the operand stage
+    const int grp = kop / C::B_ROWS, rr = kop % C::B_ROWS;
+    const int n0 = qn * 16;
+    const uint32_t base = grp * C::B_SBO + (n0 / C::B_ATOM_N) * C::B_LBO + rr * 128;
+    const int chunk0 = (n0 % C::B_ATOM_N) * (V == kFP16 ? 2 : 4) / 16;  // 16-byte chunk in the row
+    if constexpr (V == kFP16) {
+      uint32_t hp[8], lp[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        hp[j] = cvt_f16x2<R>(x[2 * j], x[2 * j + 1]);
+        float h0, h1, r0, r1;
+        unpack_f16x2(hp[j], h0, h1);
+        sm100::residual_x2(x[2 * j], x[2 * j + 1], h0, h1, scale, r0, r1);
+        lp[j] = cvt_f16x2<R>(r0, r1);
+      }
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const uint32_t off = base + (((chunk0 + q) ^ rr) << 4);
+        *reinterpret_cast<uint4*>(opBhi + off) = make_uint4(hp[4 * q], hp[4 * q + 1], hp[4 * q + 2], hp[4 * q + 3]);
+        *reinterpret_cast<uint4*>(opBlo + off) = make_uint4(lp[4 * q], lp[4 * q + 1], lp[4 * q + 2], lp[4 * q + 3]);
+      }
+    } else {
+      float hf[16], lf[16];
+#pragma unroll
+      for (int j = 0; j < 16; j += 2) {
+        hf[j] = __uint_as_float(tf32_round_bits<R>(__float_as_uint(x[j])));
+        hf[j + 1] = __uint_as_float(tf32_round_bits<R>(__float_as_uint(x[j + 1])));
+        float r0, r1;
+        sm100::residual_x2(x[j], x[j + 1], hf[j], hf[j + 1], 1.0f, r0, r1);
+        lf[j] = __uint_as_float(tf32_round_bits<R>(__float_as_uint(r0)));
+        lf[j + 1] = __uint_as_float(tf32_round_bits<R>(__float_as_uint(r1)));
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        // SWIZZLE_128B_BASE32B: 32-byte chunk index XOR (row & 3)
+        const int c16 = chunk0 + q;
+        const uint32_t off = base + ((((c16 >> 1) ^ rr) & 3) << 5) + ((c16 & 1) << 4);
+        *reinterpret_cast<float4*>(opBhi + off) = make_float4(hf[4 * q], hf[4 * q + 1], hf[4 * q + 2], hf[4 * q + 3]);
+        *reinterpret_cast<float4*>(opBlo + off) = make_float4(lf[4 * q], lf[4 * q + 1], lf[4 * q + 2], lf[4 * q + 3]);
+      }
+    }
+  }
+}
+
+template <int V, int R, bool kFlags>
+__device__ __forceinline__ void pair_split_loop(uint8_t* smem, uint64_t* stg_full,
+                                                uint64_t* stg_empty, uint64_t* op_full,
+                                                uint64_t* op_empty, int nop, int t, int lane,
+                                                float scale, FlagAcc& fa) {
+  using C = PairCfg<V>;
+  using VC = VarCfg<V>;
+  for (int kb = 0; kb < nop; ++kb) {
+    const int o = kb % C::NOP;
+    sm100::mbar_wait(&op_empty[o], ((kb / C::NOP) & 1) ^ 1);
+    uint8_t* op = smem + C::OFF_OP + o * C::OP_BYTES;
+#pragma unroll
+    for (int sub = 0; sub < VC::STG_PER_OP; ++sub) {
+      const int st = kb * VC::STG_PER_OP + sub;
+      const int s = st % C::NSTG;
+      sm100::mbar_wait(&stg_full[s], (st / C::NSTG) & 1);
+      pair_split_slice<V, R, kFlags>(smem + C::OFF_STG + s * C::STG_BYTES, op, sub, t, scale, fa);
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&stg_empty[s]);
+    }
+    sm100::fence_proxy_async_smem();
+    __syncwarp();
+    // the leader CTA's MMA thread consumes both CTAs' operand stages
+    if (lane == 0) sm100::mbar_arrive_cluster(sm100::mapa_shared(sm100::smem_u32(&op_full[o]), 0));
+  }
+}
+
+template <int V, int R>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THREADS, 1)
+    tcec_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,  // A [m][k], box 32 x 128, SW128
+                          const __grid_constant__ CUtensorMap tmB,  // B [k][n], box 32 x 32, SW128
+                          const __grid_constant__ CUtensorMap tmC,  // C [m][n], box 32 x 32, SW128
+                          const GemmShape shp, const float scale, const float inv_scale,
+                          const FlagThresholds thr, uint32_t* __restrict__ flags) {
+  using C = PairCfg<V>;
+  using VC = VarCfg<V>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* stg_full = bars;
+  uint64_t* stg_empty = bars + C::NSTG;
+  uint64_t* op_full = bars + 2 * C::NSTG;
+  uint64_t* op_empty = op_full + C::NOP;
+  uint64_t* p_full = op_empty + C::NOP;
+  uint64_t* p_empty = p_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NUM_BARS);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = sm100::cluster_ctarank();
+
+  // ---- pair tile (grouped rasterisation along m)
+  const int tiles_m = (shp.m + 2 * C::BM - 1) / (2 * C::BM);
+  const int tiles_n = (shp.n + C::BN - 1) / C::BN;
+  int tile_m, tile_n;
+  {
+    const int pid = blockIdx.x >> 1;
+    const int per_group = shp.group_m * tiles_n;
+    const int g = pid / per_group;
+    const int first_m = g * shp.group_m;
+    const int gsize = min(tiles_m - first_m, shp.group_m);
+    const int in_g = pid - g * per_group;
+    tile_m = first_m + in_g % gsize;
+    tile_n = in_g / gsize;
+  }
+  const int m_cta = tile_m * 2 * C::BM + rank * C::BM;   // this CTA's A / C rows
+  const int n_pair = tile_n * C::BN;                      // C columns of the pair
+  const int n_cta = n_pair + rank * C::BN_CTA;            // this CTA's B columns
+  const int nop = shp.num_op_stages;
+  const int nstg = nop * VC::STG_PER_OP;
+  const int de = shp.drain_every;
+
+  if (warp == 0 && lane == 0) {
+    sm100::tma_prefetch_desc(&tmA);
+    sm100::tma_prefetch_desc(&tmB);
+    sm100::tma_prefetch_desc(&tmC);
+    for (int s = 0; s < C::NSTG; ++s) {
+      sm100::mbar_init(&stg_full[s], 1);
+      sm100::mbar_init(&stg_empty[s], C::NUM_SPLIT_WARPS);
+    }
+    for (int o = 0; o < C::NOP; ++o) {
+      sm100::mbar_init(&op_full[o], 2 * C::NUM_SPLIT_WARPS);  // both CTAs' split warps
+      sm100::mbar_init(&op_empty[o], 1);
+    }
+    sm100::mbar_init(p_full, 1);
+    sm100::mbar_init(p_empty, 2 * C::NUM_DRAIN_WARPS);         // both CTAs' drain warps
+    sm100::fence_mbar_init();
+  }
+  if (warp == 2) sm100::tmem_alloc_pair<C::TMEM_COLS>(tmem_slot);
+  sm100::tc_fence_before();
+  sm100::cluster_sync();
+  sm100::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tmem_P = tmem_base;
+  const uint32_t tmem_dC = tmem_base + C::BN;
+
+  if (warp < 4) {
+    sm100::regs_dec<32>();
+    if (warp == 0 && lane == 0) {
+      // ===================== TMA producer =====================
+      for (int st = 0; st < nstg; ++st) {
+        const int s = st % C::NSTG;
+        sm100::mbar_wait(&stg_empty[s], ((st / C::NSTG) & 1) ^ 1);
+        uint8_t* dst = smem + C::OFF_STG + s * C::STG_BYTES;
+        sm100::mbar_arrive_expect_tx(&stg_full[s], C::STG_BYTES);
+        sm100::tma_load_2d(dst, &tmA, &stg_full[s], st * C::BK_STG, m_cta);
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          sm100::tma_load_2d(dst + C::STG_A_BYTES + b * C::STG_B_BOX, &tmB, &stg_full[s],
+                             n_cta + 32 * b, st * C::BK_STG);
+      }
+    } else if (warp == 1 && lane == 0 && rank == 0) {
+      // ===================== MMA issuer (leader CTA) =====================
+      constexpr uint32_t idesc = sm100::umma_idesc_bmn(VC::AB_FORMAT, 2 * C::BM, C::BN);
+      constexpr uint64_t kB = C::B_KSTEP_BYTES >> 4;
+      for (int kb = 0; kb < nop; ++kb) {
+        const int o = kb % C::NOP;
+        sm100::mbar_wait_cluster(&op_full[o], (kb / C::NOP) & 1);
+        sm100::tc_fence_after();
+        const uint32_t op = sm100::smem_u32(smem + C::OFF_OP + o * C::OP_BYTES);
+        const uint64_t a_hi = sm100::umma_desc_sw128_kmajor(op);
+        const uint64_t a_lo = sm100::umma_desc_sw128_kmajor(op + C::OP_A_BYTES);
+        const uint64_t b_hi = sm100::umma_desc_mnmajor(op + 2 * C::OP_A_BYTES, C::B_LBO, C::B_SBO, C::B_LAYOUT);
+        const uint64_t b_lo = sm100::umma_desc_mnmajor(op + 2 * C::OP_A_BYTES + C::OP_B_BYTES, C::B_LBO, C::B_SBO, C::B_LAYOUT);
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+          const uint64_t aa = static_cast<uint64_t>(ks * 2);
+          const uint64_t bb = static_cast<uint64_t>(ks) * kB;
+          sm100::mma_pair<V == kTF32>(tmem_dC, a_lo + aa, b_hi + bb, idesc, (kb | ks) != 0);
+          sm100::mma_pair<V == kTF32>(tmem_dC, a_hi + aa, b_lo + bb, idesc, 1u);
+        }
+        const bool first_in_interval = (kb % de) == 0;
+        if (first_in_interval && kb > 0) {
+          sm100::mbar_wait_cluster(p_empty, ((kb / de) - 1) & 1);
+          sm100::tc_fence_after();
+        }
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+          const uint64_t aa = static_cast<uint64_t>(ks * 2);
+          const uint64_t bb = static_cast<uint64_t>(ks) * kB;
+          sm100::mma_pair<V == kTF32>(tmem_P, a_hi + aa, b_hi + bb, idesc,
+                                      !(first_in_interval && ks == 0));
+        }
+        sm100::mma_commit_pair_mc(&op_empty[o], 0x3);
+        if ((kb % de) == de - 1 || kb == nop - 1) sm100::mma_commit_pair_mc(p_full, 0x3);
+      }
+    }
+  } else if (warp < C::DRAIN_WARP0) {
+    sm100::regs_dec<56>();
+    // ===================== split warps =====================
+    const int t = threadIdx.x - C::SPLIT_WARP0 * 32;
+    FlagAcc fa;
+    // A flags from the tile_n == 0 column of tiles, B flags from tile_m == 0:
+    // every input element is classified exactly once across the grid.
+    const bool do_flags = flags != nullptr && (tile_n == 0 || tile_m == 0);
+    if (do_flags) {
+      pair_split_loop<V, R, true>(smem, stg_full, stg_empty, op_full, op_empty, nop, t, lane, scale, fa);
+      flag_publish(fa, thr, flags);
+    } else {
+      pair_split_loop<V, R, false>(smem, stg_full, stg_empty, op_full, op_empty, nop, t, lane, scale, fa);
+    }
+  } else {
+    sm100::regs_inc<168>();
+    // ===================== drain + epilogue =====================
+    const int q = warp & 3;
+    const int h = (warp - C::DRAIN_WARP0) >> 2;
+    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+    const uint32_t p_empty_leader = sm100::mapa_shared(sm100::smem_u32(p_empty), 0);
+    float acc[128];
+#pragma unroll
+    for (int j = 0; j < 128; ++j) acc[j] = 0.0f;
+    const int nintervals = (nop + de - 1) / de;
+    for (int it = 0; it < nintervals; ++it) {
+      sm100::mbar_wait(p_full, it & 1);
+      sm100::tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        uint32_t r[16];
+        sm100::tmem_ld_32x32b_x16(tmem_P + lane_off + h * 128 + c * 16, r);
+        sm100::tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[c * 16 + j] = __fadd_rn(acc[c * 16 + j], __uint_as_float(r[j]));
+      }
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive_cluster(p_empty_leader);
+    }
+    // every MMA of the pair has completed (the last p_full commit follows them)
+    bool nonfinite = false;
+    uint8_t* stage = smem + (warp - C::DRAIN_WARP0) * C::EPI_WARP_BYTES;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      uint8_t* box = stage + b * 4096;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t r[16];
+        sm100::tmem_ld_32x32b_x16(tmem_dC + lane_off + h * 128 + b * 32 + c * 16, r);
+        sm100::tmem_ld_wait();
+        float o[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          // schemes.py:306-307: one rounding of c + dC * 2^-s
+          o[j] = __fmaf_rn(__uint_as_float(r[j]), inv_scale, acc[b * 32 + c * 16 + j]);
+          nonfinite |= !isfinite(o[j]);
+        }
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+          *reinterpret_cast<float4*>(box + sw128(lane, c * 4 + v)) =
+              make_float4(o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
+      }
+      sm100::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        sm100::tma_store_2d(&tmC, box, n_pair + h * 128 + b * 32, m_cta + q * 32);
+        sm100::tma_store_commit();
+      }
+    }
+    if (lane == 0) sm100::tma_store_wait0();
+    if (flags != nullptr && __any_sync(0xFFFFFFFFu, nonfinite) && lane == 0)
+      atomicOr(flags, kFlagOverflow);
+    sm100::tc_fence_before();
+  }
+
+  __syncthreads();
+  sm100::cluster_sync();
+  if (warp == 2) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc_pair<C::TMEM_COLS>(tmem_base);
+  }
+}
+
+}  // namespace tcec
