@@ -12,7 +12,8 @@ import os
 import subprocess
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtcec.so")
+# TCEC_LIB may point at a measurement build of the same library (make -C csrc exp)
+LIB_PATH = os.environ.get("TCEC_LIB") or os.path.join(_HERE, "libtcec.so")
 CSRC = os.path.join(_HERE, "csrc")
 
 # constants mirrored from include/tcec.h

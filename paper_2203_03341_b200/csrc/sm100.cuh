@@ -23,6 +23,27 @@ __device__ __forceinline__ uint32_t lane_id() {
   return r;
 }
 
+// ------------------------------------------------------- shared-memory I/O --
+// Explicit shared-window accesses on 32-bit addresses (never generic LD/ST).
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
+                                       uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
+               "r"(d)
+               : "memory");
+}
+__device__ __forceinline__ void sts128f(uint32_t addr, float a, float b, float c, float d) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c),
+               "f"(d)
+               : "memory");
+}
+
 // ---------------------------------------------------------------- mbarrier --
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
@@ -79,6 +100,14 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* m, uin
       " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
+}
+
+// Warm L2 with a tile the TMA will load later (no shared memory, no barrier).
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* m, int32_t c0, int32_t c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(c0), "r"(c1)
+               : "memory");
 }
 
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, const void* src, int32_t c0,
@@ -216,6 +245,26 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
                : "memory");
 }
 
+// Arrive on an mbarrier in another CTA of the cluster with the default
+// (CTA-scope release) semantics -- no GPU-scope fence.  Used where the arrive
+// only has to order this thread's completed TMEM reads, not memory writes.
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+// (a, b) += (c, d) on the f32x2 pipe, round-to-nearest.
+__device__ __forceinline__ void fadd2_rn(float& a, float& b, float c, float d) {
+  asm("{\n"
+      ".reg .b64 x, y;\n"
+      "mov.b64 x, {%0, %1};\n"
+      "mov.b64 y, {%2, %3};\n"
+      "add.rn.f32x2 x, x, y;\n"
+      "mov.b64 {%0, %1}, x;\n"
+      "}\n"
+      : "+f"(a), "+f"(b)
+      : "f"(c), "f"(d));
+}
+
 // Wait with acquire at cluster scope (for barriers that peer CTAs arrive on).
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
@@ -271,6 +320,46 @@ __device__ __forceinline__ void mma_pair(uint32_t d_tmem, uint64_t adesc, uint64
   }
 }
 
+// Same, with each descriptor given as (low, high) 32-bit halves so the issuer
+// keeps only 32-bit state in registers.
+template <bool kTF32>
+__device__ __forceinline__ void mma_pair_split(uint32_t d_tmem, uint32_t a_lo, uint32_t a_hi,
+                                               uint32_t b_lo, uint32_t b_hi, uint32_t idesc,
+                                               uint32_t accumulate) {
+  if constexpr (kTF32) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        ".reg .b64 ad, bd;\n"
+        "mov.b64 ad, {%1, %2};\n"
+        "mov.b64 bd, {%3, %4};\n"
+        "setp.ne.b32 p, %6, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], ad, bd, %5, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(accumulate)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        ".reg .b64 ad, bd;\n"
+        "mov.b64 ad, {%1, %2};\n"
+        "mov.b64 bd, {%3, %4};\n"
+        "setp.ne.b32 p, %6, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], ad, bd, %5, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(accumulate)
+        : "memory");
+  }
+}
+
+// Hide a value from the optimiser (stops it hoisting per-stage descriptor
+// math for every ring slot into registers).
+__device__ __forceinline__ uint32_t opaque(uint32_t x) {
+  asm volatile("mov.b32 %0, %0;" : "+r"(x));
+  return x;
+}
+
 // Arrive on the mbarrier at this offset in every CTA of `cta_mask` once all
 // prior tcgen05 ops of the pair have completed.
 __device__ __forceinline__ void mma_commit_pair_mc(uint64_t* bar, uint16_t cta_mask) {
@@ -312,6 +401,20 @@ __host__ __device__ constexpr uint32_t umma_idesc_bmn(uint32_t ab_format, uint32
 }
 
 // ------------------------------------------------------------- packed FP32 --
+// (x0 - h0, x1 - h1) on the f32x2 pipe (exact for the split residual).
+__device__ __forceinline__ void sub_x2(float x0, float x1, float h0, float h1, float& r0,
+                                       float& r1) {
+  asm("{\n"
+      ".reg .b64 xv, hv, rv;\n"
+      "mov.b64 xv, {%2, %3};\n"
+      "mov.b64 hv, {%4, %5};\n"
+      "sub.rn.f32x2 rv, xv, hv;\n"
+      "mov.b64 {%0, %1}, rv;\n"
+      "}\n"
+      : "=f"(r0), "=f"(r1)
+      : "f"(x0), "f"(x1), "f"(h0), "f"(h1));
+}
+
 // (x0, x1) * s and fma((h0, h1), t, (y0, y1)) on the sm_100 f32x2 pipe.
 __device__ __forceinline__ void residual_x2(float x0, float x1, float h0, float h1, float s,
                                             float& r0, float& r1) {

@@ -21,6 +21,12 @@
 
 #include "tcec_gemm.cuh"
 
+// Measurement-only builds (make exp): 1 = split warps store constants instead of
+// splitting (MMA/drain ceiling), 2 = drain warps skip the TMEM reads, 3 = both.
+#ifndef TCEC_EXP
+#define TCEC_EXP 0
+#endif
+
 namespace tcec {
 
 template <int V>
@@ -51,7 +57,7 @@ struct PairCfg {
   static constexpr int OFF_OP = NSTG * STG_BYTES;
   static constexpr int OFF_BAR = OFF_OP + NOP * OP_BYTES;
   static constexpr int NUM_BARS = 2 * NSTG + 2 * NOP + 2;
-  static constexpr int SMEM_BYTES = OFF_BAR + NUM_BARS * 8 + 16 + 1024;
+  static constexpr int SMEM_BYTES = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr int TMEM_COLS = 512;                    // P [0,256) | dC [256,512)
   static constexpr int NUM_THREADS = 640;
   static constexpr int SPLIT_WARP0 = 4, NUM_SPLIT_WARPS = 8;
@@ -63,158 +69,138 @@ struct PairCfg {
 };
 
 // Split one 32-deep FP32 slice of this CTA's A rows and B columns into the
-// operand stage.  Thread t (0..255):
+// operand stage (all addresses are 32-bit shared-window addresses).
+// Thread t (0..255):
 //   A: row r = t & 127, k in [16 (t >> 7), +16)        -> K-major hi / lo
 //   B: k = t & 31, n in [16 (t >> 5), +16)             -> MN-major hi / lo
 // With kFlags the thread also folds its inputs into the RunFlags accumulator
 // (only the CTAs designated to cover each element of A / B exactly once).
-template <int V, int R, bool kFlags>
-__device__ __forceinline__ void pair_split_slice(const uint8_t* stg, uint8_t* op, int sub, int t,
-                                                 float scale, FlagAcc& fa) {
-  using C = PairCfg<V>;
-  uint8_t* opAhi = op;
-  uint8_t* opAlo = op + C::OP_A_BYTES;
-  uint8_t* opBhi = op + 2 * C::OP_A_BYTES;
-  uint8_t* opBlo = opBhi + C::OP_B_BYTES;
-
-  // ------------------------------------------------------------------ A
-  {
-    const int r = t & 127;
-    const int half = t >> 7;
-    float x[16];
+// 16 consecutive values -> hi / lo operand words (FP16: 8 packed half2 each;
+// TF32: 16 floats each, stored as their bit patterns).
+template <int V, int R>
+__device__ __forceinline__ void split16(const float (&x)[16], float scale, uint32_t (&hw)[16],
+                                        uint32_t (&lw)[16]) {
+  if constexpr (V == kFP16) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float4 v = *reinterpret_cast<const float4*>(stg + sw128(r, half * 4 + i));
-      x[4 * i] = v.x;
-      x[4 * i + 1] = v.y;
-      x[4 * i + 2] = v.z;
-      x[4 * i + 3] = v.w;
+    for (int j = 0; j < 8; ++j) {
+      hw[j] = cvt_f16x2<R>(x[2 * j], x[2 * j + 1]);
+      float h0, h1, r0, r1;
+      unpack_f16x2(hw[j], h0, h1);
+      sm100::residual_x2(x[2 * j], x[2 * j + 1], h0, h1, scale, r0, r1);
+      lw[j] = cvt_f16x2<R>(r0, r1);
     }
-    if constexpr (kFlags) {
+  } else {
 #pragma unroll
-      for (int i = 0; i < 16; ++i) fa.add(x[i]);
-    }
-    if constexpr (V == kFP16) {
-      uint32_t hp[8], lp[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        hp[j] = cvt_f16x2<R>(x[2 * j], x[2 * j + 1]);
-        float h0, h1, r0, r1;
-        unpack_f16x2(hp[j], h0, h1);
-        sm100::residual_x2(x[2 * j], x[2 * j + 1], h0, h1, scale, r0, r1);
-        lp[j] = cvt_f16x2<R>(r0, r1);
-      }
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const uint32_t off = sw128(r, sub * 4 + half * 2 + q);
-        *reinterpret_cast<uint4*>(opAhi + off) = make_uint4(hp[4 * q], hp[4 * q + 1], hp[4 * q + 2], hp[4 * q + 3]);
-        *reinterpret_cast<uint4*>(opAlo + off) = make_uint4(lp[4 * q], lp[4 * q + 1], lp[4 * q + 2], lp[4 * q + 3]);
-      }
-    } else {
-      float hf[16], lf[16];
-#pragma unroll
-      for (int j = 0; j < 16; j += 2) {
-        hf[j] = __uint_as_float(tf32_round_bits<R>(__float_as_uint(x[j])));
-        hf[j + 1] = __uint_as_float(tf32_round_bits<R>(__float_as_uint(x[j + 1])));
-        float r0, r1;
-        sm100::residual_x2(x[j], x[j + 1], hf[j], hf[j + 1], 1.0f, r0, r1);
-        lf[j] = __uint_as_float(tf32_round_bits<R>(__float_as_uint(r0)));
-        lf[j + 1] = __uint_as_float(tf32_round_bits<R>(__float_as_uint(r1)));
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint32_t off = sw128(r, half * 4 + q);
-        *reinterpret_cast<float4*>(opAhi + off) = make_float4(hf[4 * q], hf[4 * q + 1], hf[4 * q + 2], hf[4 * q + 3]);
-        *reinterpret_cast<float4*>(opAlo + off) = make_float4(lf[4 * q], lf[4 * q + 1], lf[4 * q + 2], lf[4 * q + 3]);
-      }
+    for (int j = 0; j < 16; j += 2) {
+      hw[j] = tf32_round_bits<R>(__float_as_uint(x[j]));
+      hw[j + 1] = tf32_round_bits<R>(__float_as_uint(x[j + 1]));
+      float r0, r1;
+      sm100::sub_x2(x[j], x[j + 1], __uint_as_float(hw[j]), __uint_as_float(hw[j + 1]), r0, r1);
+      lw[j] = tf32_round_bits<R>(__float_as_uint(r0));
+      lw[j + 1] = tf32_round_bits<R>(__float_as_uint(r1));
     }
   }
-  // ------------------------------------------------------------------ B
-  {
-    const int k = t & 31;
-    const int qn = t >> 5;                 // 16-column group
-    const uint8_t* box = stg + C::STG_A_BYTES + (qn >> 1) * C::STG_B_BOX;
-    float x[16];
+}
+
+// Split this thread's share of one 32-deep FP32 slice into the operand stage.
+//   kB = false: A row t & 127, k in [16 (t >> 7), +16) -> K-major SW128 hi / lo
+//   kB = true:  B k-row t & 31, n in [16 (t >> 5), +16) -> MN-major hi / lo
+//               (SW128 for FP16, SW128_BASE32B for TF32)
+// With kFlags the inputs are folded into the RunFlags accumulator (only the
+// CTAs designated to classify each element of A / B exactly once).
+template <int V, int R, bool kFlags, bool kB>
+__device__ __forceinline__ void pair_split_part(uint32_t stg, uint32_t op, int sub, int t,
+                                                float scale, FlagAcc& fa) {
+  using C = PairCfg<V>;
+  float x[16];
+  uint32_t row, chunk_first;
+  if constexpr (!kB) {
+    row = t & 127;
+    const int half = t >> 7;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const float4 v = *reinterpret_cast<const float4*>(box + sw128(k, (qn & 1) * 4 + i));
-      x[4 * i] = v.x;
-      x[4 * i + 1] = v.y;
-      x[4 * i + 2] = v.z;
-      x[4 * i + 3] = v.w;
+      const float4 v = sm100::lds128(stg + sw128(row, half * 4 + i));
+      x[4 * i] = v.x; x[4 * i + 1] = v.y; x[4 * i + 2] = v.z; x[4 * i + 3] = v.w;
     }
-    if constexpr (kFlags) {
+    chunk_first = V == kFP16 ? sub * 4 + half * 2 : half * 4;
+  } else {
+    row = t & 31;  // k within the slice
+    const int qn = t >> 5;
+    const uint32_t box = stg + C::STG_A_BYTES + (qn >> 1) * C::STG_B_BOX;
 #pragma unroll
-      for (int i = 0; i < 16; ++i) fa.add(x[i]);
+    for (int i = 0; i < 4; ++i) {
+      const float4 v = sm100::lds128(box + sw128(row, (qn & 1) * 4 + i));
+      x[4 * i] = v.x; x[4 * i + 1] = v.y; x[4 * i + 2] = v.z; x[4 * i + 3] = v.w;
     }
-    const int kop = sub * 32 + k;          // k within the operand stage
+    chunk_first = ((qn * 16) % C::B_ATOM_N) * (V == kFP16 ? 2 : 4) / 16;
+  }
+  if constexpr (kFlags) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) fa.add(x[i]);
+  }
+  const uint32_t hi_base = op + (kB ? 2 * C::OP_A_BYTES : 0);
+  const uint32_t lo_base = hi_base + (kB ? C::OP_B_BYTES : C::OP_A_BYTES);
+#if TCEC_EXP & 1
+  sm100::sts128(hi_base + sw128(t & 127, sub * 4 + (t >> 7) * 2), 0x3c003c00u, 0, 0, 0);
+  sm100::sts128(lo_base + sw128(t & 127, sub * 4 + (t >> 7) * 2), 0x3c003c00u, 0, 0, 0);
+  return;
+#endif
+  uint32_t hw[16], lw[16];
+  split16<V, R>(x, scale, hw, lw);
+  constexpr int NCH = V == kFP16 ? 2 : 4;  // 16-byte chunks per 16 values
+  if constexpr (!kB) {
+#pragma unroll
+    for (int q = 0; q < NCH; ++q) {
+      const uint32_t off = sw128(row, chunk_first + q);
+      sm100::sts128(hi_base + off, hw[4 * q], hw[4 * q + 1], hw[4 * q + 2], hw[4 * q + 3]);
+      sm100::sts128(lo_base + off, lw[4 * q], lw[4 * q + 1], lw[4 * q + 2], lw[4 * q + 3]);
+    }
+  } else {
+    const int kop = sub * 32 + row;  // k within the operand stage
     const int grp = kop / C::B_ROWS, rr = kop % C::B_ROWS;
-    const int n0 = qn * 16;
-    const uint32_t base = grp * C::B_SBO + (n0 / C::B_ATOM_N) * C::B_LBO + rr * 128;
-    const int chunk0 = (n0 % C::B_ATOM_N) * (V == kFP16 ? 2 : 4) / 16;  // 16-byte chunk in the row
-    if constexpr (V == kFP16) {
-      uint32_t hp[8], lp[8];
+    const uint32_t base = grp * C::B_SBO + (((t >> 5) * 16) / C::B_ATOM_N) * C::B_LBO + rr * 128;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        hp[j] = cvt_f16x2<R>(x[2 * j], x[2 * j + 1]);
-        float h0, h1, r0, r1;
-        unpack_f16x2(hp[j], h0, h1);
-        sm100::residual_x2(x[2 * j], x[2 * j + 1], h0, h1, scale, r0, r1);
-        lp[j] = cvt_f16x2<R>(r0, r1);
-      }
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const uint32_t off = base + (((chunk0 + q) ^ rr) << 4);
-        *reinterpret_cast<uint4*>(opBhi + off) = make_uint4(hp[4 * q], hp[4 * q + 1], hp[4 * q + 2], hp[4 * q + 3]);
-        *reinterpret_cast<uint4*>(opBlo + off) = make_uint4(lp[4 * q], lp[4 * q + 1], lp[4 * q + 2], lp[4 * q + 3]);
-      }
-    } else {
-      float hf[16], lf[16];
-#pragma unroll
-      for (int j = 0; j < 16; j += 2) {
-        hf[j] = __uint_as_float(tf32_round_bits<R>(__float_as_uint(x[j])));
-        hf[j + 1] = __uint_as_float(tf32_round_bits<R>(__float_as_uint(x[j + 1])));
-        float r0, r1;
-        sm100::residual_x2(x[j], x[j + 1], hf[j], hf[j + 1], 1.0f, r0, r1);
-        lf[j] = __uint_as_float(tf32_round_bits<R>(__float_as_uint(r0)));
-        lf[j + 1] = __uint_as_float(tf32_round_bits<R>(__float_as_uint(r1)));
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        // SWIZZLE_128B_BASE32B: 32-byte chunk index XOR (row & 3)
-        const int c16 = chunk0 + q;
-        const uint32_t off = base + ((((c16 >> 1) ^ rr) & 3) << 5) + ((c16 & 1) << 4);
-        *reinterpret_cast<float4*>(opBhi + off) = make_float4(hf[4 * q], hf[4 * q + 1], hf[4 * q + 2], hf[4 * q + 3]);
-        *reinterpret_cast<float4*>(opBlo + off) = make_float4(lf[4 * q], lf[4 * q + 1], lf[4 * q + 2], lf[4 * q + 3]);
-      }
+    for (int q = 0; q < NCH; ++q) {
+      const int c16 = chunk_first + q;
+      // FP16 SW128: 16-byte chunk ^ row; TF32 SW128_BASE32B: 32-byte chunk ^ (row & 3)
+      const uint32_t off = V == kFP16 ? base + ((c16 ^ rr) << 4)
+                                      : base + ((((c16 >> 1) ^ rr) & 3) << 5) + ((c16 & 1) << 4);
+      sm100::sts128(hi_base + off, hw[4 * q], hw[4 * q + 1], hw[4 * q + 2], hw[4 * q + 3]);
+      sm100::sts128(lo_base + off, lw[4 * q], lw[4 * q + 1], lw[4 * q + 2], lw[4 * q + 3]);
     }
   }
 }
 
 template <int V, int R, bool kFlags>
-__device__ __forceinline__ void pair_split_loop(uint8_t* smem, uint64_t* stg_full,
+__device__ __forceinline__ void pair_split_loop(uint32_t smem, uint64_t* stg_full,
                                                 uint64_t* stg_empty, uint64_t* op_full,
                                                 uint64_t* op_empty, int nop, int t, int lane,
                                                 float scale, FlagAcc& fa) {
   using C = PairCfg<V>;
   using VC = VarCfg<V>;
+  // the leader CTA's MMA thread consumes both CTAs' operand stages
+  const uint32_t leader_op_full = sm100::mapa_shared(sm100::smem_u32(op_full), 0);
   for (int kb = 0; kb < nop; ++kb) {
     const int o = kb % C::NOP;
-    sm100::mbar_wait(&op_empty[o], ((kb / C::NOP) & 1) ^ 1);
-    uint8_t* op = smem + C::OFF_OP + o * C::OP_BYTES;
+    const uint32_t op = smem + C::OFF_OP + o * C::OP_BYTES;
 #pragma unroll
     for (int sub = 0; sub < VC::STG_PER_OP; ++sub) {
       const int st = kb * VC::STG_PER_OP + sub;
       const int s = st % C::NSTG;
       sm100::mbar_wait(&stg_full[s], (st / C::NSTG) & 1);
-      pair_split_slice<V, R, kFlags>(smem + C::OFF_STG + s * C::STG_BYTES, op, sub, t, scale, fa);
+      if (sub == 0) sm100::mbar_wait(&op_empty[o], ((kb / C::NOP) & 1) ^ 1);
+      const uint32_t stg = smem + C::OFF_STG + s * C::STG_BYTES;
+      pair_split_part<V, R, kFlags, false>(stg, op, sub, t, scale, fa);
+      pair_split_part<V, R, kFlags, true>(stg, op, sub, t, scale, fa);
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(&stg_empty[s]);
     }
+    // generic-proxy stores -> async proxy (tensor core), then signal the leader
+    // (CTA-scope release on the peer barrier, as CUTLASS's 2-SM transform
+    // pipelines do)
     sm100::fence_proxy_async_smem();
     __syncwarp();
-    // the leader CTA's MMA thread consumes both CTAs' operand stages
-    if (lane == 0) sm100::mbar_arrive_cluster(sm100::mapa_shared(sm100::smem_u32(&op_full[o]), 0));
+    if (lane == 0) sm100::mbar_arrive_remote(leader_op_full + o * 8);
   }
 }
 
@@ -227,16 +213,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
                           const FlagThresholds thr, uint32_t* __restrict__ flags) {
   using C = PairCfg<V>;
   using VC = VarCfg<V>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte alignment (SW128 atoms); identical offsets in both CTAs of the pair
+  extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
-  uint64_t* stg_full = bars;
-  uint64_t* stg_empty = bars + C::NSTG;
-  uint64_t* op_full = bars + 2 * C::NSTG;
-  uint64_t* op_empty = op_full + C::NOP;
-  uint64_t* p_full = op_empty + C::NOP;
-  uint64_t* p_empty = p_full + 1;
+  uint64_t* stg_full = bars;                    // TMA -> split          (local)
+  uint64_t* stg_empty = bars + C::NSTG;         // split -> TMA          (local, 8)
+  uint64_t* op_full = bars + 2 * C::NSTG;       // split -> MMA          (leader, 16)
+  uint64_t* op_empty = op_full + C::NOP;        // MMA commit -> split   (both, multicast)
+  uint64_t* p_full = op_empty + C::NOP;         // MMA commit -> drain   (both, multicast)
+  uint64_t* p_empty = p_full + 1;               // drain -> MMA          (leader, 16)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NUM_BARS);
+  const uint32_t smem_base = sm100::smem_u32(smem);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -262,8 +249,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
   const int nop = shp.num_op_stages;
   const int nstg = nop * VC::STG_PER_OP;
   const int de = shp.drain_every;
+  const int nintervals = (nop + de - 1) / de;
 
   if (warp == 0 && lane == 0) {
+    if (smem_base & 1023u) __trap();  // SW128 operand atoms need 1024-byte alignment
     sm100::tma_prefetch_desc(&tmA);
     sm100::tma_prefetch_desc(&tmB);
     sm100::tma_prefetch_desc(&tmC);
@@ -272,11 +261,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
       sm100::mbar_init(&stg_empty[s], C::NUM_SPLIT_WARPS);
     }
     for (int o = 0; o < C::NOP; ++o) {
-      sm100::mbar_init(&op_full[o], 2 * C::NUM_SPLIT_WARPS);  // both CTAs' split warps
+      sm100::mbar_init(&op_full[o], 2 * C::NUM_SPLIT_WARPS);
       sm100::mbar_init(&op_empty[o], 1);
     }
     sm100::mbar_init(p_full, 1);
-    sm100::mbar_init(p_empty, 2 * C::NUM_DRAIN_WARPS);         // both CTAs' drain warps
+    sm100::mbar_init(p_empty, 2 * C::NUM_DRAIN_WARPS);
     sm100::fence_mbar_init();
   }
   if (warp == 2) sm100::tmem_alloc_pair<C::TMEM_COLS>(tmem_slot);
@@ -288,10 +277,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
   const uint32_t tmem_dC = tmem_base + C::BN;
 
   if (warp < 4) {
-    sm100::regs_dec<32>();
+    sm100::regs_dec<40>();
     if (warp == 0 && lane == 0) {
       // ===================== TMA producer =====================
+      // L2 prefetch runs kPrefetch slices ahead of the staging ring so the ring's
+      // loads hit L2 instead of paying DRAM latency.
+      constexpr int kPrefetch = 6;
+      auto prefetch = [&](int sp) {
+        if (sp < nstg) {
+          sm100::tma_prefetch_2d(&tmA, sp * C::BK_STG, m_cta);
+#pragma unroll
+          for (int b = 0; b < 4; ++b) sm100::tma_prefetch_2d(&tmB, n_cta + 32 * b, sp * C::BK_STG);
+        }
+      };
+      for (int sp = C::NSTG; sp < C::NSTG + kPrefetch; ++sp) prefetch(sp);
       for (int st = 0; st < nstg; ++st) {
+        if (st >= C::NSTG) prefetch(st + kPrefetch);
         const int s = st % C::NSTG;
         sm100::mbar_wait(&stg_empty[s], ((st / C::NSTG) & 1) ^ 1);
         uint8_t* dst = smem + C::OFF_STG + s * C::STG_BYTES;
@@ -305,22 +306,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
     } else if (warp == 1 && lane == 0 && rank == 0) {
       // ===================== MMA issuer (leader CTA) =====================
       constexpr uint32_t idesc = sm100::umma_idesc_bmn(VC::AB_FORMAT, 2 * C::BM, C::BN);
-      constexpr uint64_t kB = C::B_KSTEP_BYTES >> 4;
+      // descriptor high words: SBO | version 1 | layout (K-major A: SW128; MN-major B)
+      constexpr uint32_t a_hi_w = (1024u >> 4) | (1u << 14) | (2u << 29);
+      constexpr uint32_t b_hi_w = (uint32_t(C::B_SBO) >> 4) | (1u << 14) | (C::B_LAYOUT << 29);
+      constexpr uint32_t b_lbo_w = (uint32_t(C::B_LBO) >> 4) << 16;
+      constexpr uint32_t kB = C::B_KSTEP_BYTES >> 4;
       for (int kb = 0; kb < nop; ++kb) {
         const int o = kb % C::NOP;
         sm100::mbar_wait_cluster(&op_full[o], (kb / C::NOP) & 1);
         sm100::tc_fence_after();
-        const uint32_t op = sm100::smem_u32(smem + C::OFF_OP + o * C::OP_BYTES);
-        const uint64_t a_hi = sm100::umma_desc_sw128_kmajor(op);
-        const uint64_t a_lo = sm100::umma_desc_sw128_kmajor(op + C::OP_A_BYTES);
-        const uint64_t b_hi = sm100::umma_desc_mnmajor(op + 2 * C::OP_A_BYTES, C::B_LBO, C::B_SBO, C::B_LAYOUT);
-        const uint64_t b_lo = sm100::umma_desc_mnmajor(op + 2 * C::OP_A_BYTES + C::OP_B_BYTES, C::B_LBO, C::B_SBO, C::B_LAYOUT);
+        const uint32_t op = sm100::opaque(smem_base + C::OFF_OP + o * C::OP_BYTES) >> 4;
+        const uint32_t ahi = op | (1u << 16);                                   // LBO = 16 B
+        const uint32_t alo = ahi + (C::OP_A_BYTES >> 4);
+        const uint32_t bhi = (op + ((2 * C::OP_A_BYTES) >> 4)) | b_lbo_w;
+        const uint32_t blo = bhi + (C::OP_B_BYTES >> 4);
+        // correction terms first (reference order per k-step: dA*B then A*dB) so the
+        // drain of the previous P overlaps them (schemes.py:294-298)
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {
-          const uint64_t aa = static_cast<uint64_t>(ks * 2);
-          const uint64_t bb = static_cast<uint64_t>(ks) * kB;
-          sm100::mma_pair<V == kTF32>(tmem_dC, a_lo + aa, b_hi + bb, idesc, (kb | ks) != 0);
-          sm100::mma_pair<V == kTF32>(tmem_dC, a_hi + aa, b_lo + bb, idesc, 1u);
+          sm100::mma_pair_split<V == kTF32>(tmem_dC, alo + 2 * ks, a_hi_w, bhi + kB * ks, b_hi_w,
+                                            idesc, (kb | ks) != 0);
+          sm100::mma_pair_split<V == kTF32>(tmem_dC, ahi + 2 * ks, a_hi_w, blo + kB * ks, b_hi_w,
+                                            idesc, 1u);
         }
         const bool first_in_interval = (kb % de) == 0;
         if (first_in_interval && kb > 0) {
@@ -329,10 +336,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
         }
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {
-          const uint64_t aa = static_cast<uint64_t>(ks * 2);
-          const uint64_t bb = static_cast<uint64_t>(ks) * kB;
-          sm100::mma_pair<V == kTF32>(tmem_P, a_hi + aa, b_hi + bb, idesc,
-                                      !(first_in_interval && ks == 0));
+          sm100::mma_pair_split<V == kTF32>(tmem_P, ahi + 2 * ks, a_hi_w, bhi + kB * ks, b_hi_w,
+                                            idesc, !(first_in_interval && ks == 0));
         }
         sm100::mma_commit_pair_mc(&op_empty[o], 0x3);
         if ((kb % de) == de - 1 || kb == nop - 1) sm100::mma_commit_pair_mc(p_full, 0x3);
@@ -347,13 +352,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
     // every input element is classified exactly once across the grid.
     const bool do_flags = flags != nullptr && (tile_n == 0 || tile_m == 0);
     if (do_flags) {
-      pair_split_loop<V, R, true>(smem, stg_full, stg_empty, op_full, op_empty, nop, t, lane, scale, fa);
+      pair_split_loop<V, R, true>(smem_base, stg_full, stg_empty, op_full, op_empty, nop, t, lane, scale, fa);
       flag_publish(fa, thr, flags);
     } else {
-      pair_split_loop<V, R, false>(smem, stg_full, stg_empty, op_full, op_empty, nop, t, lane, scale, fa);
+      pair_split_loop<V, R, false>(smem_base, stg_full, stg_empty, op_full, op_empty, nop, t, lane, scale, fa);
     }
   } else {
-    sm100::regs_inc<168>();
+    sm100::regs_inc<160>();
     // ===================== drain + epilogue =====================
     const int q = warp & 3;
     const int h = (warp - C::DRAIN_WARP0) >> 2;
@@ -362,28 +367,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
     float acc[128];
 #pragma unroll
     for (int j = 0; j < 128; ++j) acc[j] = 0.0f;
-    const int nintervals = (nop + de - 1) / de;
     for (int it = 0; it < nintervals; ++it) {
       sm100::mbar_wait(p_full, it & 1);
       sm100::tc_fence_after();
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
+      for (int c = 0; c < ((TCEC_EXP & 2) ? 0 : 8); ++c) {
         uint32_t r[16];
         sm100::tmem_ld_32x32b_x16(tmem_P + lane_off + h * 128 + c * 16, r);
         sm100::tmem_ld_wait();
 #pragma unroll
-        for (int j = 0; j < 16; ++j) acc[c * 16 + j] = __fadd_rn(acc[c * 16 + j], __uint_as_float(r[j]));
+        for (int j = 0; j < 16; ++j)  // schemes.py:300-304: c = RN32(c + partial)
+          acc[c * 16 + j] = __fadd_rn(acc[c * 16 + j], __uint_as_float(r[j]));
       }
       sm100::tc_fence_before();
       __syncwarp();
-      if (lane == 0) sm100::mbar_arrive_cluster(p_empty_leader);
+      // the TMEM reads above have completed (wait::ld); P may be overwritten
+      if (lane == 0) sm100::mbar_arrive_remote(p_empty_leader);
     }
     // every MMA of the pair has completed (the last p_full commit follows them)
     bool nonfinite = false;
-    uint8_t* stage = smem + (warp - C::DRAIN_WARP0) * C::EPI_WARP_BYTES;
+    const uint32_t stage = smem_base + (warp - C::DRAIN_WARP0) * C::EPI_WARP_BYTES;
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
-      uint8_t* box = stage + b * 4096;
+      const uint32_t box = stage + b * 4096;
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         uint32_t r[16];
@@ -398,13 +404,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
         }
 #pragma unroll
         for (int v = 0; v < 4; ++v)
-          *reinterpret_cast<float4*>(box + sw128(lane, c * 4 + v)) =
-              make_float4(o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
+          sm100::sts128f(box + sw128(lane, c * 4 + v), o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
       }
       sm100::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-        sm100::tma_store_2d(&tmC, box, n_pair + h * 128 + b * 32, m_cta + q * 32);
+        sm100::tma_store_2d(&tmC, smem + (box - smem_base), n_pair + h * 128 + b * 32, m_cta + q * 32);
         sm100::tma_store_commit();
       }
     }
