@@ -272,52 +272,102 @@ int tcec_sgemm(int variant, int64_t m, int64_t n, int64_t k, const float* A, int
 int tcec_sgemm_host(int variant, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda,
                     const float* B, int64_t ldb, float* C, int64_t ldc, const tcec_opts* opts,
                     uint32_t* h_flags, void* stream) {
+  // Host buffers: B goes to the device once; A and C stream through in row
+  // chunks on two copy streams so the H2D of chunk i+1 and the D2H of chunk
+  // i-1 overlap the GEMM of chunk i (rows are independent: results are
+  // bit-identical to one launch over all rows).
   if (m < 0 || n < 0 || k < 0) return TCEC_ERR_ARG;
   if (lda < (k > 0 ? k : 1) || ldb < (n > 0 ? n : 1) || ldc < (n > 0 ? n : 1)) return TCEC_ERR_ARG;
   if (h_flags) *h_flags = 0;
   if (m == 0 || n == 0) return TCEC_OK;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return TCEC_ERR_CUDA;
+  static std::once_flag pool_once[64];
+  if (dev < 64) {
+    std::call_once(pool_once[dev], [dev] {
+      // keep freed blocks cached in the stream-ordered pool between calls
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      }
+    });
+  }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  // device copies with 16-byte aligned rows
   const int64_t dlda = ((k > 0 ? k : 1) + 3) / 4 * 4;
   const int64_t dldb = (n + 3) / 4 * 4;
   const int64_t dldc = dldb;
+  const int64_t kk = k > 0 ? k : 1;
+  // chunks of rows: a multiple of the 256-row pair tile, at most 8 chunks
+  int64_t chunk = ((m + 7) / 8 + 255) / 256 * 256;
+  if (chunk < 256) chunk = 256;
+  const int nchunks = static_cast<int>((m + chunk - 1) / chunk);
   float *dA = nullptr, *dB = nullptr, *dC = nullptr;
   uint32_t* dF = nullptr;
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  cudaEvent_t ev_b = nullptr;
+  cudaEvent_t ev_in[8] = {}, ev_mm[8] = {};
   int status = TCEC_OK;
   auto cu = [&](cudaError_t e) {
     if (e != cudaSuccess && status == TCEC_OK) status = TCEC_ERR_CUDA;
     return e == cudaSuccess;
   };
-  const size_t bytesA = static_cast<size_t>(m) * dlda * sizeof(float);
-  const size_t bytesB = static_cast<size_t>(k > 0 ? k : 1) * dldb * sizeof(float);
-  const size_t bytesC = static_cast<size_t>(m) * dldc * sizeof(float);
-  if (cu(cudaMallocAsync(reinterpret_cast<void**>(&dA), bytesA, st)) &&
-      cu(cudaMallocAsync(reinterpret_cast<void**>(&dB), bytesB, st)) &&
-      cu(cudaMallocAsync(reinterpret_cast<void**>(&dC), bytesC, st)) &&
-      cu(cudaMallocAsync(reinterpret_cast<void**>(&dF), sizeof(uint32_t), st)) &&
-      cu(cudaMemsetAsync(dF, 0, sizeof(uint32_t), st))) {
-    bool ok = true;
-    if (k > 0) {
-      ok = cu(cudaMemcpy2DAsync(dA, dlda * sizeof(float), A, lda * sizeof(float),
-                                k * sizeof(float), m, cudaMemcpyHostToDevice, st)) &&
-           cu(cudaMemcpy2DAsync(dB, dldb * sizeof(float), B, ldb * sizeof(float),
-                                n * sizeof(float), k, cudaMemcpyHostToDevice, st));
-    }
-    if (ok) {
-      const int s = tcec_sgemm(variant, m, n, k, dA, dlda, dB, dldb, dC, dldc, opts, dF, st);
-      if (s != TCEC_OK) status = s;
-    }
-    if (status == TCEC_OK) {
-      cu(cudaMemcpy2DAsync(C, ldc * sizeof(float), dC, dldc * sizeof(float), n * sizeof(float), m,
-                           cudaMemcpyDeviceToHost, st));
-      if (h_flags) cu(cudaMemcpyAsync(h_flags, dF, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-    }
+  bool ok = cu(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking)) &&
+            cu(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking)) &&
+            cu(cudaEventCreateWithFlags(&ev_b, cudaEventDisableTiming));
+  for (int c = 0; ok && c < nchunks; ++c)
+    ok = cu(cudaEventCreateWithFlags(&ev_in[c], cudaEventDisableTiming)) &&
+         cu(cudaEventCreateWithFlags(&ev_mm[c], cudaEventDisableTiming));
+  ok = ok && cu(cudaMallocAsync(reinterpret_cast<void**>(&dA), size_t(m) * dlda * sizeof(float), st)) &&
+       cu(cudaMallocAsync(reinterpret_cast<void**>(&dB), size_t(kk) * dldb * sizeof(float), st)) &&
+       cu(cudaMallocAsync(reinterpret_cast<void**>(&dC), size_t(m) * dldc * sizeof(float), st)) &&
+       cu(cudaMallocAsync(reinterpret_cast<void**>(&dF), sizeof(uint32_t), st)) &&
+       cu(cudaMemsetAsync(dF, 0, sizeof(uint32_t), st));
+  if (ok && k > 0) {
+    ok = cu(cudaMemcpy2DAsync(dB, dldb * sizeof(float), B, ldb * sizeof(float), n * sizeof(float), k,
+                              cudaMemcpyHostToDevice, st)) &&
+         cu(cudaEventRecord(ev_b, st));
   }
+  if (ok) ok = cu(cudaStreamWaitEvent(s_in, ev_b, 0));  // allocations are ordered on st
+  for (int c = 0; ok && c < nchunks; ++c) {
+    const int64_t r0 = c * chunk;
+    const int64_t rows = (r0 + chunk <= m) ? chunk : m - r0;
+    if (k > 0)
+      ok = cu(cudaMemcpy2DAsync(dA + r0 * dlda, dlda * sizeof(float), A + r0 * lda,
+                                lda * sizeof(float), k * sizeof(float), rows,
+                                cudaMemcpyHostToDevice, s_in));
+    ok = ok && cu(cudaEventRecord(ev_in[c], s_in)) && cu(cudaStreamWaitEvent(st, ev_in[c], 0));
+    if (!ok) break;
+    const int s = tcec_sgemm(variant, rows, n, k, dA + r0 * dlda, dlda, dB, dldb, dC + r0 * dldc,
+                             dldc, opts, dF, st);
+    if (s != TCEC_OK) {
+      status = s;
+      ok = false;
+      break;
+    }
+    ok = cu(cudaEventRecord(ev_mm[c], st)) && cu(cudaStreamWaitEvent(s_out, ev_mm[c], 0)) &&
+         cu(cudaMemcpy2DAsync(C + r0 * ldc, ldc * sizeof(float), dC + r0 * dldc,
+                              dldc * sizeof(float), n * sizeof(float), rows,
+                              cudaMemcpyDeviceToHost, s_out));
+  }
+  if (ok && h_flags) {
+    cu(cudaStreamWaitEvent(s_out, ev_mm[nchunks - 1], 0));
+    cu(cudaMemcpyAsync(h_flags, dF, sizeof(uint32_t), cudaMemcpyDeviceToHost, s_out));
+  }
+  if (s_out) cu(cudaStreamSynchronize(s_out));
+  if (s_in) cu(cudaStreamSynchronize(s_in));
   if (dA) cudaFreeAsync(dA, st);
   if (dB) cudaFreeAsync(dB, st);
   if (dC) cudaFreeAsync(dC, st);
   if (dF) cudaFreeAsync(dF, st);
   cu(cudaStreamSynchronize(st));
+  for (int c = 0; c < nchunks; ++c) {
+    if (ev_in[c]) cudaEventDestroy(ev_in[c]);
+    if (ev_mm[c]) cudaEventDestroy(ev_mm[c]);
+  }
+  if (ev_b) cudaEventDestroy(ev_b);
+  if (s_in) cudaStreamDestroy(s_in);
+  if (s_out) cudaStreamDestroy(s_out);
   return status;
 }
 

@@ -270,13 +270,16 @@ def gemm_device(a, b, scheme="corrected3_halfhalf", cfg: MmaConfig | None = None
     return out
 
 
-def gemm(a, b, scheme, cfg: MmaConfig | None = None) -> GemmRun:
+def gemm(a, b, scheme, cfg: MmaConfig | None = None, out=None) -> GemmRun:
     """schemes.py:317-373 for the corrected3 schemes, on the GPU.
 
     numpy / array-like inputs: host buffers in, numpy float32 output (copies
-    through the C ABI's host entry, tcec_sgemm_host).  CUDA tensors: device
-    buffers, CUDA tensor output.  Either way the call synchronises once to read
-    the RunFlags, as the reference's GemmRun carries them.
+    through the C ABI's host entry, tcec_sgemm_host, which pipelines row chunks
+    of A and C against the kernel).  CUDA tensors: device buffers, CUDA tensor
+    output.  Either way the call synchronises once to read the RunFlags, as the
+    reference's GemmRun carries them.  `out` (optional) receives C: a C-contiguous
+    float32 ndarray (e.g. in pinned memory) for host inputs, a CUDA tensor for
+    device inputs.
     """
     variant, rounding, scale = resolve_scheme(scheme)
     block_k = cfg.block_k if cfg is not None else 16
@@ -290,7 +293,7 @@ def gemm(a, b, scheme, cfg: MmaConfig | None = None) -> GemmRun:
         a32 = a if a.dtype == torch.float32 else a.to(torch.float32)
         b32 = b if b.dtype == torch.float32 else b.to(torch.float32)
         fl = torch.zeros(1, dtype=torch.int32, device=a.device)
-        out = gemm_device(a32, b32, scheme, cfg, flags=fl)
+        out = gemm_device(a32, b32, scheme, cfg, out=out, flags=fl)
         m, k = a.shape
         n = b.shape[1]
         return GemmRun(m=m, n=n, k=k, scheme=scheme, output=out,
@@ -303,7 +306,13 @@ def gemm(a, b, scheme, cfg: MmaConfig | None = None) -> GemmRun:
         raise ValueError(f"inner dimensions differ: {k} vs {kb}")
     A = np.ascontiguousarray(A)
     B = np.ascontiguousarray(B)
-    C = np.empty((m, n), dtype=np.float32)
+    if out is not None:
+        if not (isinstance(out, np.ndarray) and out.dtype == np.float32 and out.shape == (m, n)
+                and out.flags["C_CONTIGUOUS"]):
+            raise ValueError("out must be a C-contiguous float32 array of shape (m, n)")
+        C = out
+    else:
+        C = np.empty((m, n), dtype=np.float32)
     fl = ctypes.c_uint32(0)
     opts = N.make_opts(split_rounding=rounding, scale_log2=scale,
                        drain_k=drain_k_for(variant, block_k))
