@@ -55,8 +55,9 @@ typedef struct tcec_opts {
   int32_t drain_k;
   /* Output tile width: 0 = default (256: CTA-pair 256 x 256 tile); 128 = single-CTA 128 x 128. */
   int32_t block_n;
-  /* Tile rasterisation group along m: 0 = default (16). */
+  /* Tile rasterisation group along m in 128-row tiles: 0 = default (8). */
   int32_t group_m;
+  /* reserved[0]: L2 prefetch distance in 32-deep k-slices (0 = off); rest must be 0. */
   int32_t reserved[3];
 } tcec_opts;
 

@@ -16,6 +16,7 @@
 #include "tcec.h"
 #include "tcec_gemm.cuh"
 #include "tcec_gemm2.cuh"
+#include "tcec_gemm3.cuh"
 
 namespace {
 
@@ -95,6 +96,7 @@ int launch_gemm(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, co
   shp.num_op_stages = static_cast<int32_t>((k + VC::BK_OP - 1) / VC::BK_OP);
   shp.drain_every = drain_every;
   shp.group_m = group_m;
+  shp.prefetch = 0;
   const float scale = ldexpf(1.0f, scale_log2);
   const float inv_scale = ldexpf(1.0f, -scale_log2);
   const tcec::FlagThresholds thr = tcec::flag_thresholds(V, R, scale_log2);
@@ -105,10 +107,10 @@ int launch_gemm(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, co
   return cudaGetLastError() == cudaSuccess ? TCEC_OK : TCEC_ERR_CUDA;
 }
 
-template <int V, int R>
+template <int V, int R, bool kUnified>
 int launch_gemm_pair(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, const float* B,
                      int64_t ldb, float* C, int64_t ldc, int scale_log2, int drain_every,
-                     int group_m, uint32_t* d_flags, cudaStream_t stream) {
+                     int group_m, int prefetch, uint32_t* d_flags, cudaStream_t stream) {
   using Cfg = tcec::PairCfg<V>;
   using VC = tcec::VarCfg<V>;
   CUtensorMap tmA, tmB, tmC;
@@ -118,7 +120,7 @@ int launch_gemm_pair(int64_t m, int64_t n, int64_t k, const float* A, int64_t ld
   if ((st = make_tmap(&tmB, B, n, k, ldb, 32, Cfg::BK_STG, CU_TENSOR_MAP_SWIZZLE_128B))) return st;
   if ((st = make_tmap(&tmC, C, n, m, ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B))) return st;
 
-  auto kern = tcec::tcec_gemm_pair_kernel<V, R>;
+  auto kern = kUnified ? tcec::tcec_gemm_pair_uni_kernel<V, R> : tcec::tcec_gemm_pair_kernel<V, R>;
   static std::once_flag attr_once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(attr_once, [&] {
@@ -134,6 +136,7 @@ int launch_gemm_pair(int64_t m, int64_t n, int64_t k, const float* A, int64_t ld
   shp.num_op_stages = static_cast<int32_t>((k + VC::BK_OP - 1) / VC::BK_OP);
   shp.drain_every = drain_every;
   shp.group_m = group_m;
+  shp.prefetch = prefetch;
   const float scale = ldexpf(1.0f, scale_log2);
   const float inv_scale = ldexpf(1.0f, -scale_log2);
   const tcec::FlagThresholds thr = tcec::flag_thresholds(V, R, scale_log2);
@@ -146,12 +149,15 @@ int launch_gemm_pair(int64_t m, int64_t n, int64_t k, const float* A, int64_t ld
 
 template <int V, int R>
 int dispatch_bn(int bn, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda,
-                const float* B, int64_t ldb, float* C, int64_t ldc, int s, int de, int gm,
-                uint32_t* fl, cudaStream_t st) {
+                const float* B, int64_t ldb, float* C, int64_t ldc, int s, int de, int gm, int pf,
+                int kv, uint32_t* fl, cudaStream_t st) {
   switch (bn) {
     case 256:
-      return launch_gemm_pair<V, R>(m, n, k, A, lda, B, ldb, C, ldc, s, de, gm / 2 > 0 ? gm / 2 : 1,
-                                    fl, st);
+      if (kv == 1)
+        return launch_gemm_pair<V, R, true>(m, n, k, A, lda, B, ldb, C, ldc, s, de,
+                                            gm / 2 > 0 ? gm / 2 : 1, pf, fl, st);
+      return launch_gemm_pair<V, R, false>(m, n, k, A, lda, B, ldb, C, ldc, s, de,
+                                           gm / 2 > 0 ? gm / 2 : 1, pf, fl, st);
     case 128:
       return launch_gemm<V, R, 128>(m, n, k, A, lda, B, ldb, C, ldc, s, de, gm, fl, st);
     default:
@@ -234,7 +240,11 @@ int tcec_sgemm(int variant, int64_t m, int64_t n, int64_t k, const float* A, int
   }
   const int block_n = o.block_n == 0 ? 256 : o.block_n;
   if (block_n != 128 && block_n != 256) return TCEC_ERR_UNSUPPORTED;
-  const int group_m = o.group_m <= 0 ? 16 : o.group_m;
+  const int group_m = o.group_m <= 0 ? 8 : o.group_m;
+  // reserved[0]: L2 prefetch distance in 32-deep k-slices (pair kernel; 0 = off)
+  const int prefetch = o.reserved[0] < 0 ? 0 : (o.reserved[0] > 16 ? 16 : o.reserved[0]);
+  // reserved[1]: pair-kernel variant (0 = split + drain warps, 1 = unified split/drain workers)
+  const int kvariant = o.reserved[1];
   if (m == 0 || n == 0) return TCEC_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (k == 0) {
@@ -251,21 +261,21 @@ int tcec_sgemm(int variant, int64_t m, int64_t n, int64_t k, const float* A, int
   if (variant == TCEC_FP16) {
     if (rounding == TCEC_ROUND_RN)
       return dispatch_bn<tcec::kFP16, tcec::kRN>(block_n, m, n, k, A, lda, B, ldb, C, ldc,
-                                                 scale_log2, drain_every, group_m, d_flags, st);
+                                                 scale_log2, drain_every, group_m, prefetch, kvariant, d_flags, st);
     if (rounding == TCEC_ROUND_RZ)
       return dispatch_bn<tcec::kFP16, tcec::kRZ>(block_n, m, n, k, A, lda, B, ldb, C, ldc,
-                                                 scale_log2, drain_every, group_m, d_flags, st);
+                                                 scale_log2, drain_every, group_m, prefetch, kvariant, d_flags, st);
     return TCEC_ERR_UNSUPPORTED;
   }
   if (rounding == TCEC_ROUND_RNA)
     return dispatch_bn<tcec::kTF32, tcec::kRNA>(block_n, m, n, k, A, lda, B, ldb, C, ldc, 0,
-                                                drain_every, group_m, d_flags, st);
+                                                drain_every, group_m, prefetch, kvariant, d_flags, st);
   if (rounding == TCEC_ROUND_RN)
     return dispatch_bn<tcec::kTF32, tcec::kRN>(block_n, m, n, k, A, lda, B, ldb, C, ldc, 0,
-                                               drain_every, group_m, d_flags, st);
+                                               drain_every, group_m, prefetch, kvariant, d_flags, st);
   if (rounding == TCEC_ROUND_RZ)
     return dispatch_bn<tcec::kTF32, tcec::kRZ>(block_n, m, n, k, A, lda, B, ldb, C, ldc, 0,
-                                               drain_every, group_m, d_flags, st);
+                                               drain_every, group_m, prefetch, kvariant, d_flags, st);
   return TCEC_ERR_UNSUPPORTED;
 }
 

@@ -31,6 +31,7 @@ struct GemmShape {
   int32_t num_op_stages;   // ceil(k / BK_OP)
   int32_t drain_every;     // operand stages per drain interval (>= 1)
   int32_t group_m;         // tile rasterisation group
+  int32_t prefetch;        // L2 prefetch distance in staging slices (0 = off)
 };
 
 template <int BN_>

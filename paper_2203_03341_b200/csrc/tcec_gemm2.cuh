@@ -282,7 +282,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
       // ===================== TMA producer =====================
       // L2 prefetch runs kPrefetch slices ahead of the staging ring so the ring's
       // loads hit L2 instead of paying DRAM latency.
-      constexpr int kPrefetch = 6;
+      const int kPrefetch = shp.prefetch;
       auto prefetch = [&](int sp) {
         if (sp < nstg) {
           sm100::tma_prefetch_2d(&tmA, sp * C::BK_STG, m_cta);
@@ -292,7 +292,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
       };
       for (int sp = C::NSTG; sp < C::NSTG + kPrefetch; ++sp) prefetch(sp);
       for (int st = 0; st < nstg; ++st) {
-        if (st >= C::NSTG) prefetch(st + kPrefetch);
+        if (kPrefetch > 0 && st >= C::NSTG) prefetch(st + kPrefetch);
         const int s = st % C::NSTG;
         sm100::mbar_wait(&stg_empty[s], ((st / C::NSTG) & 1) ^ 1);
         uint8_t* dst = smem + C::OFF_STG + s * C::STG_BYTES;
