@@ -57,7 +57,8 @@ typedef struct tcec_opts {
   int32_t block_n;
   /* Tile rasterisation group along m in 128-row tiles: 0 = default (8). */
   int32_t group_m;
-  /* reserved[0]: L2 prefetch distance in 32-deep k-slices (0 = off); rest must be 0. */
+  /* reserved[0]: L2 prefetch distance in 32-deep k-slices (0 = off);
+   * reserved[1]: pair-kernel variant (0 = split + drain warps, 1 = unified workers); rest 0. */
   int32_t reserved[3];
 } tcec_opts;
 

@@ -98,9 +98,11 @@ def check(status: int, what: str) -> None:
 
 
 def make_opts(split_rounding: int = ROUND_DEFAULT, scale_log2: int = -1, drain_k: int = 0,
-              block_n: int = 0, group_m: int = 0, prefetch: int = 0) -> TcecOpts:
+              block_n: int = 0, group_m: int = 0, prefetch: int = 0,
+              kernel_variant: int = 0) -> TcecOpts:
     o = TcecOpts()
     o.reserved[0] = prefetch
+    o.reserved[1] = kernel_variant
     o.split_rounding = split_rounding
     o.scale_log2 = scale_log2
     o.drain_k = drain_k

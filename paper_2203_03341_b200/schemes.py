@@ -228,7 +228,8 @@ def _tma_ready(t):
 
 
 def gemm_device(a, b, scheme="corrected3_halfhalf", cfg: MmaConfig | None = None, out=None,
-                flags=None, block_n: int = 0, group_m: int = 0, prefetch: int = 0):
+                flags=None, block_n: int = 0, group_m: int = 0, prefetch: int = 0,
+                kernel_variant: int = 0):
     """C = A @ B on CUDA float32 tensors, stream-ordered on torch's current stream.
 
     No host synchronisation: `flags` (int32 CUDA tensor, one element, caller
@@ -257,7 +258,7 @@ def gemm_device(a, b, scheme="corrected3_halfhalf", cfg: MmaConfig | None = None
     block_k = cfg.block_k if cfg is not None else 16
     opts = N.make_opts(split_rounding=rounding, scale_log2=scale,
                        drain_k=drain_k_for(variant, block_k), block_n=block_n, group_m=group_m,
-                       prefetch=prefetch)
+                       prefetch=prefetch, kernel_variant=kernel_variant)
     A, lda = _tma_ready(a)
     B, ldb = _tma_ready(b)
     C, ldc = out, out.stride(0)
