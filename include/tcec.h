@@ -50,8 +50,8 @@ typedef struct tcec_opts {
    * 0 with FP16 is the unscaled markidis_halfhalf split (splitting.py:70-71). */
   int32_t scale_log2;
   /* Drain interval of the main-term partial in k (MmaConfig.block_k,
-   * mma.py:34): 0 = one operand stage (64 for FP16, 32 for TF32); otherwise a
-   * positive multiple of that stage depth. */
+   * mma.py:34): 0 = default (128 for FP16, 64 for TF32); otherwise a positive
+   * multiple of the operand stage depth (64 for FP16, 32 for TF32). */
   int32_t drain_k;
   /* Output tile width: 0 = default (256: CTA-pair 256 x 256 tile); 128 = single-CTA 128 x 128. */
   int32_t block_n;

@@ -233,7 +233,9 @@ int tcec_sgemm(int variant, int64_t m, int64_t n, int64_t k, const float* A, int
   if (variant == TCEC_TF32 && scale_log2 != 0) return TCEC_ERR_UNSUPPORTED;
   if (variant == TCEC_FP16 && scale_log2 != 0 && scale_log2 != 11) return TCEC_ERR_UNSUPPORTED;
   const int bk_op = variant == TCEC_FP16 ? 64 : 32;
-  int drain_every = 1;
+  // default drain interval: 128 (FP16) / 64 (TF32) -- measured both faster and
+  // more accurate against FP64 than draining every operand stage
+  int drain_every = 2;
   if (o.drain_k != 0) {
     if (o.drain_k < 0 || o.drain_k % bk_op != 0) return TCEC_ERR_UNSUPPORTED;
     drain_every = o.drain_k / bk_op;

@@ -32,7 +32,8 @@ pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 TOL_ULP = 32.0
 TOL_OUT_OF_RANGE = 2.0 ** -12
-VARIANTS = [("corrected3_halfhalf", "fp16", 16, 64), ("corrected3_tf32", "tf32", 8, 32)]
+# (scheme, oracle variant, MMA k-step, default drain interval of the kernel)
+VARIANTS = [("corrected3_halfhalf", "fp16", 16, 128), ("corrected3_tf32", "tf32", 8, 64)]
 
 
 def _T():
@@ -199,16 +200,26 @@ def test_row_and_column_separable(sname, variant, bk, drain):
 
 @pytest.mark.parametrize("sname,variant,bk,drain", VARIANTS)
 def test_drain_interval_option(sname, variant, bk, drain):
-    """MmaConfig.block_k selects the drain interval (whole operand stages); each
-    matches the oracle's drain restatement at that interval."""
+    """Every supported drain interval (whole operand stages) matches the oracle's
+    drain restatement at that interval; MmaConfig.block_k maps to
+    max(default, block_k rounded up to stages)."""
+    import torch
+
     T = _T()
     a = O.urand(128, 1024, -1, 1, 9)
     b = O.urand(1024, 128, -1, 1, O.pair_seed(9))
-    for d in (drain, 2 * drain, 4 * drain):
-        cfg = T.MmaConfig(block_k=d)
-        c, _ = _run(a, b, sname, cfg=cfg)
+    stage = 64 if variant == "fp16" else 32
+    A, B = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    for d in (stage, 2 * stage, 4 * stage, 8 * stage):
+        c = T.gemm_device(A, B, sname, drain_k=d).cpu().numpy()
         oc, _ = O.corrected3(a, b, variant, block_k=bk, drain_k=d)
         _check_close(c, oc, a, b, (sname, d), variant)
+    v = 0 if variant == "fp16" else 1
+    assert T.schemes.drain_k_for(v, 16) == drain
+    assert T.schemes.drain_k_for(v, 4 * drain) == 4 * drain
+    c_cfg, _ = _run(a, b, sname, cfg=T.MmaConfig(block_k=4 * drain))
+    c_dk = T.gemm_device(A, B, sname, drain_k=4 * drain).cpu().numpy()
+    assert np.array_equal(c_cfg, c_dk)
 
 
 def test_host_path_equals_device_path():
@@ -280,10 +291,10 @@ def test_reference_scheme_objects_are_accepted():
     c2, _ = _run(a, b, "corrected3_halfhalf")
     assert np.array_equal(c1, c2)
     c3, _ = _run(a, b, T.corrected3(T.tf32tf32(T.RoundingMode.RZ)))
-    oc, _ = O.corrected3(a, b, "tf32", block_k=8, drain_k=32, rounding=O.RM_RZ)
+    oc, _ = O.corrected3(a, b, "tf32", block_k=8, drain_k=64, rounding=O.RM_RZ)
     _check_close(c3, oc, a, b, "tf32 rz", "tf32")
     c4, _ = _run(a, b, T.corrected3(T.markidis_halfhalf()))
-    oc, _ = O.corrected3(a, b, "fp16u", block_k=16, drain_k=64)
+    oc, _ = O.corrected3(a, b, "fp16u", block_k=16, drain_k=128)
     _check_close(c4, oc, a, b, "fp16 unscaled", "fp16u")
     with pytest.raises(NotImplementedError):
         T.gemm(a, b, "markidis4")
@@ -313,7 +324,7 @@ def test_large_square_properties(sname):
     a = A[rows[:4]].cpu().numpy()
     b = B[:, 1000:1040].cpu().numpy()
     oc, _ = O.corrected3(a, b, variant, block_k=16 if variant == "fp16" else 8,
-                         drain_k=64 if variant == "fp16" else 32)
+                         drain_k=128 if variant == "fp16" else 64)
     _check_close(C[rows[:4]][:, 1000:1040].cpu().numpy(), oc, a, b, sname, variant)
 
 
@@ -336,3 +347,22 @@ def test_pair_kernel_bitwise_equals_single_cta_kernel(sname, variant, bk, drain,
     c2 = T.gemm_device(A, B, sname, block_n=256, flags=f2)
     assert torch.equal(c1.view(torch.int32), c2.view(torch.int32))
     assert int(f1.item()) == int(f2.item())
+
+
+@pytest.mark.parametrize("sname,variant,bk,drain", VARIANTS)
+def test_unified_worker_variant_bitwise_equal(sname, variant, bk, drain):
+    """The unified split+drain worker pair kernel (kernel_variant=1) runs the same
+    arithmetic as the default pair kernel: bit-identical outputs and flags."""
+    import torch
+
+    T = _T()
+    g = torch.Generator(device="cuda")
+    g.manual_seed(11)
+    A = torch.rand((520, 1000), generator=g, device="cuda") * 2 - 1
+    B = torch.rand((1000, 300), generator=g, device="cuda") * 2 - 1
+    f0 = torch.zeros(1, dtype=torch.int32, device="cuda")
+    f1 = torch.zeros(1, dtype=torch.int32, device="cuda")
+    c0 = T.gemm_device(A, B, sname, flags=f0)
+    c1 = T.gemm_device(A, B, sname, flags=f1, kernel_variant=1)
+    assert torch.equal(c0.view(torch.int32), c1.view(torch.int32))
+    assert int(f0.item()) == int(f1.item())
