@@ -81,6 +81,19 @@ __device__ __forceinline__ uint32_t tf32_round_bits(uint32_t u) {
   }
 }
 
+// The same rounding without clearing the low 13 bits (value whose top 19 bits
+// equal tf32_round_bits); for operands consumed by the tensor core only.
+template <int R>
+__device__ __forceinline__ uint32_t tf32_carry_bits(uint32_t u) {
+  if constexpr (R == kRNA) {
+    return u + 0x1000u;
+  } else if constexpr (R == kRN) {
+    return u + 0x0FFFu + ((u >> 13) & 1u);
+  } else {
+    return u;
+  }
+}
+
 template <int R>
 __device__ __forceinline__ void split_tf32(float x, float scale, float& hi, float& lo) {
   const float h = __uint_as_float(tf32_round_bits<R>(__float_as_uint(x)));

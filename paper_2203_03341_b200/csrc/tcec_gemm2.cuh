@@ -23,6 +23,9 @@
 
 // Measurement-only builds (make exp): 1 = split warps store constants instead of
 // splitting (MMA/drain ceiling), 2 = drain warps skip the TMEM reads, 3 = both.
+#ifndef TCEC_TF32_NOMASK
+#define TCEC_TF32_NOMASK 0
+#endif
 #ifndef TCEC_EXP
 #define TCEC_EXP 0
 #endif
@@ -90,6 +93,22 @@ __device__ __forceinline__ void split16(const float (&x)[16], float scale, uint3
       lw[j] = cvt_f16x2<R>(r0, r1);
     }
   } else {
+#if TCEC_TF32_NOMASK
+    // tcgen05 kind::tf32 reads only the top 19 bits of each 32-bit operand, so
+    // the rounding carry is enough: the low 13 bits need no clearing (the
+    // residual still uses the cleared hi).  Tests check bit-identity.
+#pragma unroll
+    for (int j = 0; j < 16; j += 2) {
+      const uint32_t h0 = tf32_round_bits<R>(__float_as_uint(x[j]));
+      const uint32_t h1 = tf32_round_bits<R>(__float_as_uint(x[j + 1]));
+      hw[j] = tf32_carry_bits<R>(__float_as_uint(x[j]));
+      hw[j + 1] = tf32_carry_bits<R>(__float_as_uint(x[j + 1]));
+      float r0, r1;
+      sm100::sub_x2(x[j], x[j + 1], __uint_as_float(h0), __uint_as_float(h1), r0, r1);
+      lw[j] = tf32_carry_bits<R>(__float_as_uint(r0));
+      lw[j + 1] = tf32_carry_bits<R>(__float_as_uint(r1));
+    }
+#else
 #pragma unroll
     for (int j = 0; j < 16; j += 2) {
       hw[j] = tf32_round_bits<R>(__float_as_uint(x[j]));
@@ -99,6 +118,7 @@ __device__ __forceinline__ void split16(const float (&x)[16], float scale, uint3
       lw[j] = tf32_round_bits<R>(__float_as_uint(r0));
       lw[j + 1] = tf32_round_bits<R>(__float_as_uint(r1));
     }
+#endif
   }
 }
 

@@ -1,0 +1,73 @@
+"""Input generators (product restatement of genmat.py) against the reference's
+own outputs, and the accuracy harness CLI (CPU parts + one GPU run)."""
+
+import os
+
+import numpy as np
+import pytest
+
+from paper_2203_03341_b200 import accuracy as ACC
+from paper_2203_03341_b200 import genmat as G
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def test_generators_match_reference_fixtures():
+    g = np.load(os.path.join(GOLD, "genmat_golden.npz"))
+    assert np.array_equal(G.generate(G.MatrixSpec(4, 5, G.Urand(-1, 1), 0)), g["urand_s0"])
+    assert np.array_equal(G.generate(G.MatrixSpec(5, 3, G.Urand(-1, 1), G.pair_seed(0))),
+                          g["urand_pair_s0"])
+    assert np.array_equal(G.generate(G.MatrixSpec(6, 4, G.ExpRand(-15, 14), 3)), g["exprand_s3"])
+    for t in (1, 2, 3, 4):
+        a, b = G.type_pair(t, 3, 4, 5, 9)
+        assert np.array_equal(a, g[f"type{t}_A"]) and np.array_equal(b, g[f"type{t}_B"])
+
+
+def test_generators_match_reference_gemm_inputs():
+    """The GEMM goldens were drawn by the reference's generate(): same bits here."""
+    g = np.load(os.path.join(GOLD, "gemm_golden.npz"))
+    a = G.generate(G.MatrixSpec(16, 1024, G.Urand(-1, 1), 0))
+    b = G.generate(G.MatrixSpec(1024, 16, G.Urand(-1, 1), G.pair_seed(0)))
+    assert np.array_equal(a, g["urand_s0_16x16x1024__A"])
+    assert np.array_equal(b, g["urand_s0_16x16x1024__B"])
+
+
+def test_spec_validation():
+    with pytest.raises(ValueError):
+        G.Urand(1, 1)
+    with pytest.raises(ValueError):
+        G.ExpRand(3, 2)
+    with pytest.raises(ValueError):
+        G.MatrixSpec(0, 3, G.Urand(0, 1), 1)
+    with pytest.raises(ValueError):
+        G.type_pair(5, 2, 2, 2, 0)
+
+
+def test_parse_dist_and_cli_errors(capsys):
+    assert ACC.parse_dist("urand:-1,1") == G.Urand(-1.0, 1.0)
+    assert ACC.parse_dist("exprand:-15,14") == G.ExpRand(-15, 14)
+    assert ACC.parse_dist("type:3") == ("type", 3)
+    for bad in ("urand:1", "type:7", "gauss:0,1"):
+        with pytest.raises(ValueError):
+            ACC.parse_dist(bad)
+    assert ACC.main(["gemm-accuracy", "--scheme", "fp32_simt"]) == 1
+    assert "error:" in capsys.readouterr().err
+
+
+@pytest.mark.gpu
+def test_gemm_accuracy_csv_on_gpu(tmp_path):
+    out = tmp_path / "acc.csv"
+    rc = ACC.main(["--out", str(out), "gemm-accuracy", "--m", "16", "--n", "16", "--k", "1024",
+                   "--seeds", "0,1,2,3", "--scheme",
+                   "corrected3_halfhalf,corrected3_tf32,cublas_sgemm"])
+    assert rc == 0
+    lines = out.read_text().strip().splitlines()
+    assert lines[0] == "m,n,k,scheme,seed,residual,flags"
+    avg = {ln.split(",")[3]: float(ln.split(",")[5]) for ln in lines if ",avg," in ln}
+    assert set(avg) == {"corrected3_halfhalf", "corrected3_tf32", "cublas_sgemm"}
+    for name in ("corrected3_halfhalf", "corrected3_tf32"):
+        assert avg[name] < 4e-7
+    rc = ACC.main(["--out", str(out), "gemm-accuracy", "--k", "256", "--seeds", "0",
+                   "--scheme", "corrected3_halfhalf", "--dist", "type:4"])
+    assert rc == 0
+    assert "out_of_range" in out.read_text()
