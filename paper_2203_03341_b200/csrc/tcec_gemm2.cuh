@@ -129,6 +129,45 @@ __device__ __forceinline__ void split16(const float (&x)[16], float scale, uint3
 // With kFlags the inputs are folded into the RunFlags accumulator (only the
 // CTAs designated to classify each element of A / B exactly once).
 template <int V, int R, bool kFlags, bool kB>
+__device__ __forceinline__ void pair_split_regs(const float (&x)[16], uint32_t op, int sub, int t,
+                                                float scale, FlagAcc& fa) {
+  using C = PairCfg<V>;
+  if constexpr (kFlags) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) fa.add(x[i]);
+  }
+  const uint32_t hi_base = op + (kB ? 2 * C::OP_A_BYTES : 0);
+  const uint32_t lo_base = hi_base + (kB ? C::OP_B_BYTES : C::OP_A_BYTES);
+  uint32_t hw[16], lw[16];
+  split16<V, R>(x, scale, hw, lw);
+  constexpr int NCH = V == kFP16 ? 2 : 4;
+  if constexpr (!kB) {
+    const int row = t & 127, half = t >> 7;
+    const int chunk_first = V == kFP16 ? sub * 4 + half * 2 : half * 4;
+#pragma unroll
+    for (int q = 0; q < NCH; ++q) {
+      const uint32_t off = sw128(row, chunk_first + q);
+      sm100::sts128(hi_base + off, hw[4 * q], hw[4 * q + 1], hw[4 * q + 2], hw[4 * q + 3]);
+      sm100::sts128(lo_base + off, lw[4 * q], lw[4 * q + 1], lw[4 * q + 2], lw[4 * q + 3]);
+    }
+  } else {
+    const int row = t & 31, qn = t >> 5;
+    const int chunk_first = ((qn * 16) % C::B_ATOM_N) * (V == kFP16 ? 2 : 4) / 16;
+    const int kop = sub * 32 + row;
+    const int grp = kop / C::B_ROWS, rr = kop % C::B_ROWS;
+    const uint32_t base = grp * C::B_SBO + ((qn * 16) / C::B_ATOM_N) * C::B_LBO + rr * 128;
+#pragma unroll
+    for (int q = 0; q < NCH; ++q) {
+      const int c16 = chunk_first + q;
+      const uint32_t off = V == kFP16 ? base + ((c16 ^ rr) << 4)
+                                      : base + ((((c16 >> 1) ^ rr) & 3) << 5) + ((c16 & 1) << 4);
+      sm100::sts128(hi_base + off, hw[4 * q], hw[4 * q + 1], hw[4 * q + 2], hw[4 * q + 3]);
+      sm100::sts128(lo_base + off, lw[4 * q], lw[4 * q + 1], lw[4 * q + 2], lw[4 * q + 3]);
+    }
+  }
+}
+
+template <int V, int R, bool kFlags, bool kB>
 __device__ __forceinline__ void pair_split_part(uint32_t stg, uint32_t op, int sub, int t,
                                                 float scale, FlagAcc& fa) {
   using C = PairCfg<V>;
@@ -139,7 +178,11 @@ __device__ __forceinline__ void pair_split_part(uint32_t stg, uint32_t op, int s
     const int half = t >> 7;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
+#if TCEC_EXP & 8
+      const float4 v = make_float4(__int_as_float(t * 7 + i), 1.5f + i, 2.5f, -0.75f * half);
+#else
       const float4 v = sm100::lds128(stg + sw128(row, half * 4 + i));
+#endif
       x[4 * i] = v.x; x[4 * i + 1] = v.y; x[4 * i + 2] = v.z; x[4 * i + 3] = v.w;
     }
     chunk_first = V == kFP16 ? sub * 4 + half * 2 : half * 4;
@@ -149,7 +192,11 @@ __device__ __forceinline__ void pair_split_part(uint32_t stg, uint32_t op, int s
     const uint32_t box = stg + C::STG_A_BYTES + (qn >> 1) * C::STG_B_BOX;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
+#if TCEC_EXP & 8
+      const float4 v = make_float4(__int_as_float(t * 5 + i), 0.5f + i, 3.5f, -1.25f * qn);
+#else
       const float4 v = sm100::lds128(box + sw128(row, (qn & 1) * 4 + i));
+#endif
       x[4 * i] = v.x; x[4 * i + 1] = v.y; x[4 * i + 2] = v.z; x[4 * i + 3] = v.w;
     }
     chunk_first = ((qn * 16) % C::B_ATOM_N) * (V == kFP16 ? 2 : 4) / 16;
@@ -210,10 +257,30 @@ __device__ __forceinline__ void pair_split_loop(uint32_t smem, uint64_t* stg_ful
       sm100::mbar_wait(&stg_full[s], (st / C::NSTG) & 1);
       if (sub == 0) sm100::mbar_wait(&op_empty[o], ((kb / C::NOP) & 1) ^ 1);
       const uint32_t stg = smem + C::OFF_STG + s * C::STG_BYTES;
+#if TCEC_EXP & 16
+      {
+        // issue both parts' shared loads before converting either (more ILP)
+        float xa[16], xb[16];
+        const int r = t & 127, half = t >> 7, kk = t & 31, qn = t >> 5;
+        const uint32_t box = stg + C::STG_A_BYTES + (qn >> 1) * C::STG_B_BOX;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float4 v = sm100::lds128(stg + sw128(r, half * 4 + i));
+          xa[4 * i] = v.x; xa[4 * i + 1] = v.y; xa[4 * i + 2] = v.z; xa[4 * i + 3] = v.w;
+          const float4 u = sm100::lds128(box + sw128(kk, (qn & 1) * 4 + i));
+          xb[4 * i] = u.x; xb[4 * i + 1] = u.y; xb[4 * i + 2] = u.z; xb[4 * i + 3] = u.w;
+        }
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive(&stg_empty[s]);
+        pair_split_regs<V, R, kFlags, false>(xa, op, sub, t, scale, fa);
+        pair_split_regs<V, R, kFlags, true>(xb, op, sub, t, scale, fa);
+      }
+#else
       pair_split_part<V, R, kFlags, false>(stg, op, sub, t, scale, fa);
       pair_split_part<V, R, kFlags, true>(stg, op, sub, t, scale, fa);
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(&stg_empty[s]);
+#endif
     }
     // generic-proxy stores -> async proxy (tensor core), then signal the leader
     // (CTA-scope release on the peer barrier, as CUTLASS's 2-SM transform
@@ -316,12 +383,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
         const int s = st % C::NSTG;
         sm100::mbar_wait(&stg_empty[s], ((st / C::NSTG) & 1) ^ 1);
         uint8_t* dst = smem + C::OFF_STG + s * C::STG_BYTES;
+#if TCEC_EXP & 4
+        sm100::mbar_arrive(&stg_full[s]);
+        (void)dst;
+#else
         sm100::mbar_arrive_expect_tx(&stg_full[s], C::STG_BYTES);
         sm100::tma_load_2d(dst, &tmA, &stg_full[s], st * C::BK_STG, m_cta);
 #pragma unroll
         for (int b = 0; b < 4; ++b)
           sm100::tma_load_2d(dst + C::STG_A_BYTES + b * C::STG_B_BOX, &tmB, &stg_full[s],
                              n_cta + 32 * b, st * C::BK_STG);
+#endif
       }
     } else if (warp == 1 && lane == 0 && rank == 0) {
       // ===================== MMA issuer (leader CTA) =====================

@@ -1,0 +1,6 @@
+#!/bin/bash
+rm -f gpurun_out/exp2.log
+for L in libtcec.so libtcec_exp4.so libtcec_exp8.so libtcec_exp12.so libtcec_exp1.so; do
+  TCEC_LIB=$PWD/paper_2203_03341_b200/$L timeout 300 python scripts/perf_exp.py >> gpurun_out/exp2.log 2>&1
+done
+cat gpurun_out/exp2.log

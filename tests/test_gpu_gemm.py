@@ -349,20 +349,23 @@ def test_pair_kernel_bitwise_equals_single_cta_kernel(sname, variant, bk, drain,
     assert int(f1.item()) == int(f2.item())
 
 
+@pytest.mark.parametrize("kv", [1, 2, 3])
 @pytest.mark.parametrize("sname,variant,bk,drain", VARIANTS)
-def test_unified_worker_variant_bitwise_equal(sname, variant, bk, drain):
-    """The unified split+drain worker pair kernel (kernel_variant=1) runs the same
-    arithmetic as the default pair kernel: bit-identical outputs and flags."""
+def test_kernel_variants_bitwise_equal(sname, variant, bk, drain, kv):
+    """The pair-kernel variants (1: unified split+drain workers, 2: FP32 loaded
+    straight to registers, no staging ring) run the same per-element arithmetic
+    as the staged pair kernel: bit-identical outputs and flags, including ragged
+    edges."""
     import torch
 
     T = _T()
     g = torch.Generator(device="cuda")
     g.manual_seed(11)
-    A = torch.rand((520, 1000), generator=g, device="cuda") * 2 - 1
-    B = torch.rand((1000, 300), generator=g, device="cuda") * 2 - 1
+    A = torch.rand((520, 1004), generator=g, device="cuda") * 2 - 1
+    B = torch.rand((1004, 300), generator=g, device="cuda") * 2 - 1
     f0 = torch.zeros(1, dtype=torch.int32, device="cuda")
     f1 = torch.zeros(1, dtype=torch.int32, device="cuda")
     c0 = T.gemm_device(A, B, sname, flags=f0)
-    c1 = T.gemm_device(A, B, sname, flags=f1, kernel_variant=1)
+    c1 = T.gemm_device(A, B, sname, flags=f1, kernel_variant=kv)
     assert torch.equal(c0.view(torch.int32), c1.view(torch.int32))
     assert int(f0.item()) == int(f1.item())
