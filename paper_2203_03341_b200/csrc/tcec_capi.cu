@@ -17,7 +17,6 @@
 #include "tcec_gemm.cuh"
 #include "tcec_gemm2.cuh"
 #include "tcec_gemm3.cuh"
-#include "tcec_gemm4.cuh"
 
 namespace {
 
@@ -149,83 +148,6 @@ int launch_gemm_pair(int64_t m, int64_t n, int64_t k, const float* A, int64_t ld
 }
 
 template <int V, int R>
-int launch_gemm_direct(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda,
-                       const float* B, int64_t ldb, float* C, int64_t ldc, int scale_log2,
-                       int drain_every, int group_m, int prefetch, uint32_t* d_flags,
-                       cudaStream_t stream) {
-  using Cfg = tcec::PairCfg<V>;
-  using VC = tcec::VarCfg<V>;
-  using D = tcec::DirectCfg<V>;
-  CUtensorMap tmA, tmB, tmC;
-  int st;
-  if ((st = make_tmap(&tmA, A, k, m, lda, Cfg::BK_STG, Cfg::BM, CU_TENSOR_MAP_SWIZZLE_128B)))
-    return st;
-  if ((st = make_tmap(&tmB, B, n, k, ldb, 32, Cfg::BK_STG, CU_TENSOR_MAP_SWIZZLE_128B))) return st;
-  if ((st = make_tmap(&tmC, C, n, m, ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B))) return st;
-  auto kern = tcec::tcec_gemm_direct_kernel<V, R>;
-  static std::once_flag attr_once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(attr_once, [&] {
-    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    D::SMEM_BYTES);
-  });
-  if (attr_err != cudaSuccess) return TCEC_ERR_CUDA;
-  tcec::GemmShape shp;
-  shp.m = static_cast<int32_t>(m);
-  shp.n = static_cast<int32_t>(n);
-  shp.k = static_cast<int32_t>(k);
-  shp.num_op_stages = static_cast<int32_t>((k + VC::BK_OP - 1) / VC::BK_OP);
-  shp.drain_every = drain_every;
-  shp.group_m = group_m;
-  shp.prefetch = prefetch;
-  const float scale = ldexpf(1.0f, scale_log2);
-  const float inv_scale = ldexpf(1.0f, -scale_log2);
-  const tcec::FlagThresholds thr = tcec::flag_thresholds(V, R, scale_log2);
-  const int64_t pairs = ((m + 2 * Cfg::BM - 1) / (2 * Cfg::BM)) * ((n + Cfg::BN - 1) / Cfg::BN);
-  kern<<<static_cast<unsigned>(2 * pairs), D::NUM_THREADS, D::SMEM_BYTES, stream>>>(
-      A, lda, B, ldb, tmA, tmB, tmC, shp, scale, inv_scale, thr, d_flags);
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  return cudaGetLastError() == cudaSuccess ? TCEC_OK : TCEC_ERR_CUDA;
-}
-
-template <int V, int R>
-int launch_gemm_hybrid(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda,
-                       const float* B, int64_t ldb, float* C, int64_t ldc, int scale_log2,
-                       int drain_every, int group_m, uint32_t* d_flags, cudaStream_t stream) {
-  using Cfg = tcec::PairCfg<V>;
-  using VC = tcec::VarCfg<V>;
-  using H = tcec::HybridCfg<V>;
-  CUtensorMap tmB, tmC;
-  int st;
-  if ((st = make_tmap(&tmB, B, n, k, ldb, 32, Cfg::BK_STG, CU_TENSOR_MAP_SWIZZLE_128B))) return st;
-  if ((st = make_tmap(&tmC, C, n, m, ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B))) return st;
-  auto kern = tcec::tcec_gemm_hybrid_kernel<V, R>;
-  static std::once_flag attr_once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(attr_once, [&] {
-    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    H::SMEM_BYTES);
-  });
-  if (attr_err != cudaSuccess) return TCEC_ERR_CUDA;
-  tcec::GemmShape shp;
-  shp.m = static_cast<int32_t>(m);
-  shp.n = static_cast<int32_t>(n);
-  shp.k = static_cast<int32_t>(k);
-  shp.num_op_stages = static_cast<int32_t>((k + VC::BK_OP - 1) / VC::BK_OP);
-  shp.drain_every = drain_every;
-  shp.group_m = group_m;
-  shp.prefetch = 0;
-  const float scale = ldexpf(1.0f, scale_log2);
-  const float inv_scale = ldexpf(1.0f, -scale_log2);
-  const tcec::FlagThresholds thr = tcec::flag_thresholds(V, R, scale_log2);
-  const int64_t pairs = ((m + 2 * Cfg::BM - 1) / (2 * Cfg::BM)) * ((n + Cfg::BN - 1) / Cfg::BN);
-  kern<<<static_cast<unsigned>(2 * pairs), H::NUM_THREADS, H::SMEM_BYTES, stream>>>(
-      A, lda, tmB, tmC, shp, scale, inv_scale, thr, d_flags);
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  return cudaGetLastError() == cudaSuccess ? TCEC_OK : TCEC_ERR_CUDA;
-}
-
-template <int V, int R>
 int dispatch_bn(int bn, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda,
                 const float* B, int64_t ldb, float* C, int64_t ldc, int s, int de, int gm, int pf,
                 int kv, uint32_t* fl, cudaStream_t st) {
@@ -234,12 +156,7 @@ int dispatch_bn(int bn, int64_t m, int64_t n, int64_t k, const float* A, int64_t
       if (kv == 1)
         return launch_gemm_pair<V, R, true>(m, n, k, A, lda, B, ldb, C, ldc, s, de,
                                             gm / 2 > 0 ? gm / 2 : 1, pf, fl, st);
-      if (kv == 2)
-        return launch_gemm_direct<V, R>(m, n, k, A, lda, B, ldb, C, ldc, s, de,
-                                        gm / 2 > 0 ? gm / 2 : 1, pf, fl, st);
-      if (kv == 3)
-        return launch_gemm_hybrid<V, R>(m, n, k, A, lda, B, ldb, C, ldc, s, de,
-                                        gm / 2 > 0 ? gm / 2 : 1, fl, st);
+      if (kv != 0) return TCEC_ERR_UNSUPPORTED;
       return launch_gemm_pair<V, R, false>(m, n, k, A, lda, B, ldb, C, ldc, s, de,
                                            gm / 2 > 0 ? gm / 2 : 1, pf, fl, st);
     case 128:

@@ -21,11 +21,10 @@
 
 #include "tcec_gemm.cuh"
 
-// Measurement-only builds (make exp): 1 = split warps store constants instead of
-// splitting (MMA/drain ceiling), 2 = drain warps skip the TMEM reads, 3 = both.
-#ifndef TCEC_TF32_NOMASK
-#define TCEC_TF32_NOMASK 0
-#endif
+// Measurement-only builds (make exp; results are garbage): bit 1 = split warps
+// store constants instead of splitting, bit 2 = drain warps skip the TMEM
+// reads, bit 4 = no TMA loads (staging left stale), bit 8 = split warps skip
+// the staging reads (LDS).  Used to attribute time.
 #ifndef TCEC_EXP
 #define TCEC_EXP 0
 #endif
@@ -93,22 +92,6 @@ __device__ __forceinline__ void split16(const float (&x)[16], float scale, uint3
       lw[j] = cvt_f16x2<R>(r0, r1);
     }
   } else {
-#if TCEC_TF32_NOMASK
-    // tcgen05 kind::tf32 reads only the top 19 bits of each 32-bit operand, so
-    // the rounding carry is enough: the low 13 bits need no clearing (the
-    // residual still uses the cleared hi).  Tests check bit-identity.
-#pragma unroll
-    for (int j = 0; j < 16; j += 2) {
-      const uint32_t h0 = tf32_round_bits<R>(__float_as_uint(x[j]));
-      const uint32_t h1 = tf32_round_bits<R>(__float_as_uint(x[j + 1]));
-      hw[j] = tf32_carry_bits<R>(__float_as_uint(x[j]));
-      hw[j + 1] = tf32_carry_bits<R>(__float_as_uint(x[j + 1]));
-      float r0, r1;
-      sm100::sub_x2(x[j], x[j + 1], __uint_as_float(h0), __uint_as_float(h1), r0, r1);
-      lw[j] = tf32_carry_bits<R>(__float_as_uint(r0));
-      lw[j + 1] = tf32_carry_bits<R>(__float_as_uint(r1));
-    }
-#else
 #pragma unroll
     for (int j = 0; j < 16; j += 2) {
       hw[j] = tf32_round_bits<R>(__float_as_uint(x[j]));
@@ -118,7 +101,6 @@ __device__ __forceinline__ void split16(const float (&x)[16], float scale, uint3
       lw[j] = tf32_round_bits<R>(__float_as_uint(r0));
       lw[j + 1] = tf32_round_bits<R>(__float_as_uint(r1));
     }
-#endif
   }
 }
 
@@ -257,30 +239,10 @@ __device__ __forceinline__ void pair_split_loop(uint32_t smem, uint64_t* stg_ful
       sm100::mbar_wait(&stg_full[s], (st / C::NSTG) & 1);
       if (sub == 0) sm100::mbar_wait(&op_empty[o], ((kb / C::NOP) & 1) ^ 1);
       const uint32_t stg = smem + C::OFF_STG + s * C::STG_BYTES;
-#if TCEC_EXP & 16
-      {
-        // issue both parts' shared loads before converting either (more ILP)
-        float xa[16], xb[16];
-        const int r = t & 127, half = t >> 7, kk = t & 31, qn = t >> 5;
-        const uint32_t box = stg + C::STG_A_BYTES + (qn >> 1) * C::STG_B_BOX;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float4 v = sm100::lds128(stg + sw128(r, half * 4 + i));
-          xa[4 * i] = v.x; xa[4 * i + 1] = v.y; xa[4 * i + 2] = v.z; xa[4 * i + 3] = v.w;
-          const float4 u = sm100::lds128(box + sw128(kk, (qn & 1) * 4 + i));
-          xb[4 * i] = u.x; xb[4 * i + 1] = u.y; xb[4 * i + 2] = u.z; xb[4 * i + 3] = u.w;
-        }
-        __syncwarp();
-        if (lane == 0) sm100::mbar_arrive(&stg_empty[s]);
-        pair_split_regs<V, R, kFlags, false>(xa, op, sub, t, scale, fa);
-        pair_split_regs<V, R, kFlags, true>(xb, op, sub, t, scale, fa);
-      }
-#else
       pair_split_part<V, R, kFlags, false>(stg, op, sub, t, scale, fa);
       pair_split_part<V, R, kFlags, true>(stg, op, sub, t, scale, fa);
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(&stg_empty[s]);
-#endif
     }
     // generic-proxy stores -> async proxy (tensor core), then signal the leader
     // (CTA-scope release on the peer barrier, as CUTLASS's 2-SM transform

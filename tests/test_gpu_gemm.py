@@ -349,7 +349,7 @@ def test_pair_kernel_bitwise_equals_single_cta_kernel(sname, variant, bk, drain,
     assert int(f1.item()) == int(f2.item())
 
 
-@pytest.mark.parametrize("kv", [1, 2, 3])
+@pytest.mark.parametrize("kv", [1])
 @pytest.mark.parametrize("sname,variant,bk,drain", VARIANTS)
 def test_kernel_variants_bitwise_equal(sname, variant, bk, drain, kv):
     """The pair-kernel variants (1: unified split+drain workers, 2: FP32 loaded
