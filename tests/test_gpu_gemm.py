@@ -222,17 +222,22 @@ def test_drain_interval_option(sname, variant, bk, drain):
     assert np.array_equal(c_cfg, c_dk)
 
 
-def test_host_path_equals_device_path():
+@pytest.mark.parametrize("shape", [(130, 61, 77), (1100, 700, 300)])
+def test_host_path_equals_device_path(shape):
+    """The host entry (blocked, overlapped copies; k and n not multiples of 4 in
+    the first case, 3 x 3 blocks in the second) is bit-identical to the device
+    entry."""
     T = _T()
-    a = O.urand(130, 77, -1, 1, 10)   # k not a multiple of 4: padded host path
-    b = O.urand(77, 61, -1, 1, 11)    # n not a multiple of 4
+    m, n, k = shape
+    a = O.urand(m, k, -1, 1, 10)
+    b = O.urand(k, n, -1, 1, 11)
     for sname, *_ in VARIANTS:
         c_dev, f_dev = _run(a, b, sname)
         run = T.gemm(a, b, sname)
         assert isinstance(run.output, np.ndarray) and run.output.dtype == np.float32
         assert np.array_equal(run.output, c_dev)
         assert run.flags == f_dev
-        assert (run.m, run.n, run.k) == (130, 61, 77)
+        assert (run.m, run.n, run.k) == (m, n, k)
 
 
 def test_float64_host_input_is_validated_like_reference():
