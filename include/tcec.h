@@ -57,8 +57,15 @@ typedef struct tcec_opts {
   int32_t block_n;
   /* Tile rasterisation group along m in 128-row tiles: 0 = default (8). */
   int32_t group_m;
+  /* Where the hi/lo split runs: 0 = default, 1 = fused into the GEMM's TMA
+   * pipeline (FP32 tiles split in shared memory), 2 = split once per input
+   * element in a separate HBM pass, then a three-product GEMM over the
+   * pre-split operands (workspace 2(m + n)k operand elements, stream-ordered
+   * allocation).  Results are bit-identical. */
+  int32_t split_mode;
   /* reserved[0]: L2 prefetch distance in 32-deep k-slices (0 = off);
-   * reserved[1]: pair-kernel variant (0 = split + drain warps, 1 = unified workers); rest 0. */
+   * reserved[1]: pair-kernel variant (0 = split + drain warps, 1 = unified workers);
+   * reserved[2]: pair-kernel MMA order (0 = corrections first, 1 = A_hi collector reuse). */
   int32_t reserved[3];
 } tcec_opts;
 

@@ -353,6 +353,87 @@ __device__ __forceinline__ void mma_pair_split(uint32_t d_tmem, uint32_t a_lo, u
   }
 }
 
+// CTA-pair MMA with the A operand in tensor memory (each CTA's TMEM holds its
+// 128 rows: lane = row, column = 32-bit word of K) and B from shared memory.
+template <bool kTF32>
+__device__ __forceinline__ void mma_pair_ts(uint32_t d_tmem, uint32_t a_tmem, uint32_t b_lo,
+                                            uint32_t b_hi, uint32_t idesc, uint32_t accumulate) {
+  if constexpr (kTF32) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        ".reg .b64 bd;\n"
+        "mov.b64 bd, {%2, %3};\n"
+        "setp.ne.b32 p, %5, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], bd, %4, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(accumulate)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        ".reg .b64 bd;\n"
+        "mov.b64 bd, {%2, %3};\n"
+        "setp.ne.b32 p, %5, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], bd, %4, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(accumulate)
+        : "memory");
+  }
+}
+
+// 32 lanes x 8 / 16 consecutive 32-bit columns <- registers (one lane per thread).
+__device__ __forceinline__ void tmem_st_32x32b_x8(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+// mma_pair_split with an A-operand collector hint (kC: 0 none, 1 fill = keep A
+// for the next MMA, 2 use = reuse and keep, 3 lastuse = reuse then release).
+template <bool kTF32, int kC>
+__device__ __forceinline__ void mma_pair_col(uint32_t d_tmem, uint32_t a_lo, uint32_t a_hi,
+                                             uint32_t b_lo, uint32_t b_hi, uint32_t idesc,
+                                             uint32_t accumulate) {
+#define TCEC_MMA_COL(KIND, COL)                                                   \
+  asm volatile(                                                                   \
+      "{\n"                                                                       \
+      ".reg .pred p;\n"                                                           \
+      ".reg .b64 ad, bd;\n"                                                       \
+      "mov.b64 ad, {%1, %2};\n"                                                   \
+      "mov.b64 bd, {%3, %4};\n"                                                   \
+      "setp.ne.b32 p, %6, 0;\n"                                                   \
+      "tcgen05.mma.cta_group::2.kind::" KIND COL " [%0], ad, bd, %5, p;\n"         \
+      "}\n" ::"r"(d_tmem),                                                        \
+      "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(accumulate)     \
+      : "memory")
+  if constexpr (kTF32) {
+    if constexpr (kC == 0) TCEC_MMA_COL("tf32", "");
+    else if constexpr (kC == 1) TCEC_MMA_COL("tf32", ".collector::a::fill");
+    else if constexpr (kC == 2) TCEC_MMA_COL("tf32", ".collector::a::use");
+    else TCEC_MMA_COL("tf32", ".collector::a::lastuse");
+  } else {
+    if constexpr (kC == 0) TCEC_MMA_COL("f16", "");
+    else if constexpr (kC == 1) TCEC_MMA_COL("f16", ".collector::a::fill");
+    else if constexpr (kC == 2) TCEC_MMA_COL("f16", ".collector::a::use");
+    else TCEC_MMA_COL("f16", ".collector::a::lastuse");
+  }
+#undef TCEC_MMA_COL
+}
+
 // Hide a value from the optimiser (stops it hoisting per-stage descriptor
 // math for every ring slot into registers).
 __device__ __forceinline__ uint32_t opaque(uint32_t x) {

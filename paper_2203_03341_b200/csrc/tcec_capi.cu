@@ -17,6 +17,8 @@
 #include "tcec_gemm.cuh"
 #include "tcec_gemm2.cuh"
 #include "tcec_gemm3.cuh"
+#include "tcec_gemm4.cuh"
+#include "tcec_presplit.cuh"
 
 namespace {
 
@@ -64,6 +66,35 @@ int make_tmap(CUtensorMap* tm, const void* ptr, uint64_t inner, uint64_t outer, 
   return r == CUDA_SUCCESS ? TCEC_OK : TCEC_ERR_CUDA;
 }
 
+// 2-D tensor map over a row-major [outer][inner] operand workspace (FP16 or
+// 32-bit elements), 128-byte swizzled boxes of 128 bytes x box_outer.
+int make_tmap_op(CUtensorMap* tm, const void* ptr, CUtensorMapDataType dt, uint32_t esize,
+                 uint64_t inner, uint64_t outer, uint64_t ld_elems, uint32_t box_outer) {
+  const cuuint64_t dims[2] = {inner, outer};
+  const cuuint64_t strides[1] = {ld_elems * esize};
+  const cuuint32_t box[2] = {128u / esize, box_outer};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = g_encode(tm, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? TCEC_OK : TCEC_ERR_CUDA;
+}
+
+// Keep freed blocks cached in the device's stream-ordered pool between calls
+// (workspaces of the host path and of the split-once mode).
+void keep_pool(int dev) {
+  static std::once_flag pool_once[64];
+  if (dev < 0 || dev >= 64) return;
+  std::call_once(pool_once[dev], [dev] {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  });
+}
+
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 template <int V, int R, int BN>
@@ -97,6 +128,7 @@ int launch_gemm(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, co
   shp.drain_every = drain_every;
   shp.group_m = group_m;
   shp.prefetch = 0;
+  shp.mma_order = 0;
   const float scale = ldexpf(1.0f, scale_log2);
   const float inv_scale = ldexpf(1.0f, -scale_log2);
   const tcec::FlagThresholds thr = tcec::flag_thresholds(V, R, scale_log2);
@@ -110,7 +142,8 @@ int launch_gemm(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, co
 template <int V, int R, bool kUnified>
 int launch_gemm_pair(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, const float* B,
                      int64_t ldb, float* C, int64_t ldc, int scale_log2, int drain_every,
-                     int group_m, int prefetch, uint32_t* d_flags, cudaStream_t stream) {
+                     int group_m, int prefetch, int mma_order, uint32_t* d_flags,
+                     cudaStream_t stream) {
   using Cfg = tcec::PairCfg<V>;
   using VC = tcec::VarCfg<V>;
   CUtensorMap tmA, tmB, tmC;
@@ -137,6 +170,7 @@ int launch_gemm_pair(int64_t m, int64_t n, int64_t k, const float* A, int64_t ld
   shp.drain_every = drain_every;
   shp.group_m = group_m;
   shp.prefetch = prefetch;
+  shp.mma_order = mma_order;
   const float scale = ldexpf(1.0f, scale_log2);
   const float inv_scale = ldexpf(1.0f, -scale_log2);
   const tcec::FlagThresholds thr = tcec::flag_thresholds(V, R, scale_log2);
@@ -147,18 +181,140 @@ int launch_gemm_pair(int64_t m, int64_t n, int64_t k, const float* A, int64_t ld
   return cudaGetLastError() == cudaSuccess ? TCEC_OK : TCEC_ERR_CUDA;
 }
 
+template <int V, int R, int BN, int NOP>
+int launch_gemm_ts(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, const float* B,
+                   int64_t ldb, float* C, int64_t ldc, int scale_log2, int drain_every,
+                   int group_m, uint32_t* d_flags, cudaStream_t stream) {
+  using Cfg = tcec::TsCfg<V, BN, NOP>;
+  using VC = tcec::VarCfg<V>;
+  CUtensorMap tmA, tmB, tmC;
+  int st;
+  if ((st = make_tmap(&tmA, A, k, m, lda, Cfg::BK_STG, Cfg::BM, CU_TENSOR_MAP_SWIZZLE_128B)))
+    return st;
+  if ((st = make_tmap(&tmB, B, n, k, ldb, 32, Cfg::BK_STG, CU_TENSOR_MAP_SWIZZLE_128B))) return st;
+  if ((st = make_tmap(&tmC, C, n, m, ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B))) return st;
+
+  auto kern = tcec::tcec_gemm_ts_kernel<V, R, BN, NOP>;
+  static std::once_flag attr_once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(attr_once, [&] {
+    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    Cfg::SMEM_BYTES);
+  });
+  if (attr_err != cudaSuccess) return TCEC_ERR_CUDA;
+
+  tcec::GemmShape shp;
+  shp.m = static_cast<int32_t>(m);
+  shp.n = static_cast<int32_t>(n);
+  shp.k = static_cast<int32_t>(k);
+  shp.num_op_stages = static_cast<int32_t>((k + VC::BK_OP - 1) / VC::BK_OP);
+  shp.drain_every = drain_every;
+  shp.group_m = group_m;
+  shp.prefetch = 0;
+  shp.mma_order = 0;
+  const float scale = ldexpf(1.0f, scale_log2);
+  const float inv_scale = ldexpf(1.0f, -scale_log2);
+  const tcec::FlagThresholds thr = tcec::flag_thresholds(V, R, scale_log2);
+  const int64_t pairs = ((m + 2 * Cfg::BM - 1) / (2 * Cfg::BM)) * ((n + Cfg::BN - 1) / Cfg::BN);
+  kern<<<static_cast<unsigned>(2 * pairs), Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream>>>(
+      tmA, tmB, tmC, shp, scale, inv_scale, thr, d_flags);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError() == cudaSuccess ? TCEC_OK : TCEC_ERR_CUDA;
+}
+
+// Split-once mode: one split pass per input (A as m x k, B transposed to
+// n x k, both K-major in the operand type), then the three-product GEMM.
+template <int V, int R>
+int launch_gemm_presplit(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda,
+                         const float* B, int64_t ldb, float* C, int64_t ldc, int scale_log2,
+                         int drain_every, int group_m, uint32_t* d_flags, cudaStream_t stream) {
+  using Cfg = tcec::PsCfg<V>;
+  using VC = tcec::VarCfg<V>;
+  const uint32_t esize = V == tcec::kFP16 ? 2u : 4u;
+  const CUtensorMapDataType dt =
+      V == tcec::kFP16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  const int64_t ldk = (k + 15) / 16 * 16;
+  const size_t a_bytes = size_t(m) * ldk * esize, b_bytes = size_t(n) * ldk * esize;
+  uint8_t* ws = nullptr;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return TCEC_ERR_CUDA;
+  keep_pool(dev);
+  if (cudaMallocAsync(reinterpret_cast<void**>(&ws), 2 * (a_bytes + b_bytes), stream) != cudaSuccess)
+    return TCEC_ERR_CUDA;
+  void* ah = ws;
+  void* al = ws + a_bytes;
+  void* bh = ws + 2 * a_bytes;
+  void* bl = ws + 2 * a_bytes + b_bytes;
+  int st = TCEC_OK;
+  CUtensorMap tmAh, tmAl, tmBh, tmBl, tmC;
+  if (!st) st = make_tmap_op(&tmAh, ah, dt, esize, k, m, ldk, Cfg::BM);
+  if (!st) st = make_tmap_op(&tmAl, al, dt, esize, k, m, ldk, Cfg::BM);
+  if (!st) st = make_tmap_op(&tmBh, bh, dt, esize, k, n, ldk, Cfg::BN_CTA);
+  if (!st) st = make_tmap_op(&tmBl, bl, dt, esize, k, n, ldk, Cfg::BN_CTA);
+  if (!st) st = make_tmap(&tmC, C, n, m, ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+  auto kern = tcec::tcec_gemm_ps_kernel<V>;
+  static std::once_flag attr_once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(attr_once, [&] {
+    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    Cfg::SMEM_BYTES);
+  });
+  if (!st && attr_err != cudaSuccess) st = TCEC_ERR_CUDA;
+  if (!st) {
+    const float scale = ldexpf(1.0f, scale_log2);
+    const float inv_scale = ldexpf(1.0f, -scale_log2);
+    const tcec::FlagThresholds thr = tcec::flag_thresholds(V, R, scale_log2);
+    const unsigned ga = static_cast<unsigned>(((m + 63) / 64) * ((k + 63) / 64));
+    tcec::tcec_presplit_kernel<V, R, false><<<ga, 256, 0, stream>>>(
+        A, static_cast<int32_t>(m), static_cast<int32_t>(k), lda, ah, al, ldk,
+        static_cast<int32_t>(m), scale, thr, d_flags);
+    const unsigned gb = static_cast<unsigned>(((k + 63) / 64) * ((n + 63) / 64));
+    tcec::tcec_presplit_kernel<V, R, true><<<gb, 256, 0, stream>>>(
+        B, static_cast<int32_t>(k), static_cast<int32_t>(n), ldb, bh, bl, ldk,
+        static_cast<int32_t>(n), scale, thr, d_flags);
+    tcec::GemmShape shp;
+    shp.m = static_cast<int32_t>(m);
+    shp.n = static_cast<int32_t>(n);
+    shp.k = static_cast<int32_t>(k);
+    shp.num_op_stages = static_cast<int32_t>((k + VC::BK_OP - 1) / VC::BK_OP);
+    shp.drain_every = drain_every;
+    shp.group_m = group_m;
+    shp.prefetch = 0;
+    shp.mma_order = 0;
+    const int64_t pairs = ((m + 2 * Cfg::BM - 1) / (2 * Cfg::BM)) * ((n + Cfg::BN - 1) / Cfg::BN);
+    kern<<<static_cast<unsigned>(2 * pairs), Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream>>>(
+        tmAh, tmAl, tmBh, tmBl, tmC, shp, inv_scale, d_flags);
+    g_launches.fetch_add(3, std::memory_order_relaxed);
+    if (cudaGetLastError() != cudaSuccess) st = TCEC_ERR_CUDA;
+  }
+  cudaFreeAsync(ws, stream);
+  return st;
+}
+
 template <int V, int R>
 int dispatch_bn(int bn, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda,
                 const float* B, int64_t ldb, float* C, int64_t ldc, int s, int de, int gm, int pf,
-                int kv, uint32_t* fl, cudaStream_t st) {
+                int kv, int mo, int sm, uint32_t* fl, cudaStream_t st) {
+  if (sm == 2) {
+    if (bn != 256 || kv != 0 || mo != 0) return TCEC_ERR_UNSUPPORTED;
+    return launch_gemm_presplit<V, R>(m, n, k, A, lda, B, ldb, C, ldc, s, de,
+                                      gm / 2 > 0 ? gm / 2 : 1, fl, st);
+  }
   switch (bn) {
     case 256:
       if (kv == 1)
         return launch_gemm_pair<V, R, true>(m, n, k, A, lda, B, ldb, C, ldc, s, de,
-                                            gm / 2 > 0 ? gm / 2 : 1, pf, fl, st);
+                                            gm / 2 > 0 ? gm / 2 : 1, pf, mo, fl, st);
       if (kv != 0) return TCEC_ERR_UNSUPPORTED;
       return launch_gemm_pair<V, R, false>(m, n, k, A, lda, B, ldb, C, ldc, s, de,
-                                           gm / 2 > 0 ? gm / 2 : 1, pf, fl, st);
+                                           gm / 2 > 0 ? gm / 2 : 1, pf, mo, fl, st);
+    case 192:
+      if (kv != 0) return TCEC_ERR_UNSUPPORTED;
+      return launch_gemm_ts<V, R, 192, 2>(m, n, k, A, lda, B, ldb, C, ldc, s, de,
+                                           gm / 2 > 0 ? gm / 2 : 1, fl, st);
+    case 129:  // measurement: A-from-TMEM kernel at N = 128 with a 4-stage ring
+      return launch_gemm_ts<V, R, 128, 4>(m, n, k, A, lda, B, ldb, C, ldc, s, de,
+                                          gm / 2 > 0 ? gm / 2 : 1, fl, st);
     case 128:
       return launch_gemm<V, R, 128>(m, n, k, A, lda, B, ldb, C, ldc, s, de, gm, fl, st);
     default:
@@ -242,12 +398,18 @@ int tcec_sgemm(int variant, int64_t m, int64_t n, int64_t k, const float* A, int
     drain_every = o.drain_k / bk_op;
   }
   const int block_n = o.block_n == 0 ? 256 : o.block_n;
-  if (block_n != 128 && block_n != 256) return TCEC_ERR_UNSUPPORTED;
+  if (block_n != 128 && block_n != 129 && block_n != 192 && block_n != 256) return TCEC_ERR_UNSUPPORTED;
   const int group_m = o.group_m <= 0 ? 8 : o.group_m;
   // reserved[0]: L2 prefetch distance in 32-deep k-slices (pair kernel; 0 = off)
   const int prefetch = o.reserved[0] < 0 ? 0 : (o.reserved[0] > 16 ? 16 : o.reserved[0]);
   // reserved[1]: pair-kernel variant (0 = split + drain warps, 1 = unified split/drain workers)
   const int kvariant = o.reserved[1];
+  // reserved[2]: pair-kernel MMA order (0 = corrections then main term, 1 = A_hi collector reuse)
+  const int mma_order = o.reserved[2];
+  if (mma_order != 0 && mma_order != 1) return TCEC_ERR_UNSUPPORTED;
+  // split_mode: 0 / 1 = split fused into the GEMM, 2 = split once in a separate pass
+  const int split_mode = o.split_mode;
+  if (split_mode < 0 || split_mode > 2) return TCEC_ERR_UNSUPPORTED;
   if (m == 0 || n == 0) return TCEC_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (k == 0) {
@@ -264,21 +426,21 @@ int tcec_sgemm(int variant, int64_t m, int64_t n, int64_t k, const float* A, int
   if (variant == TCEC_FP16) {
     if (rounding == TCEC_ROUND_RN)
       return dispatch_bn<tcec::kFP16, tcec::kRN>(block_n, m, n, k, A, lda, B, ldb, C, ldc,
-                                                 scale_log2, drain_every, group_m, prefetch, kvariant, d_flags, st);
+                                                 scale_log2, drain_every, group_m, prefetch, kvariant, mma_order, split_mode, d_flags, st);
     if (rounding == TCEC_ROUND_RZ)
       return dispatch_bn<tcec::kFP16, tcec::kRZ>(block_n, m, n, k, A, lda, B, ldb, C, ldc,
-                                                 scale_log2, drain_every, group_m, prefetch, kvariant, d_flags, st);
+                                                 scale_log2, drain_every, group_m, prefetch, kvariant, mma_order, split_mode, d_flags, st);
     return TCEC_ERR_UNSUPPORTED;
   }
   if (rounding == TCEC_ROUND_RNA)
     return dispatch_bn<tcec::kTF32, tcec::kRNA>(block_n, m, n, k, A, lda, B, ldb, C, ldc, 0,
-                                                drain_every, group_m, prefetch, kvariant, d_flags, st);
+                                                drain_every, group_m, prefetch, kvariant, mma_order, split_mode, d_flags, st);
   if (rounding == TCEC_ROUND_RN)
     return dispatch_bn<tcec::kTF32, tcec::kRN>(block_n, m, n, k, A, lda, B, ldb, C, ldc, 0,
-                                               drain_every, group_m, prefetch, kvariant, d_flags, st);
+                                               drain_every, group_m, prefetch, kvariant, mma_order, split_mode, d_flags, st);
   if (rounding == TCEC_ROUND_RZ)
     return dispatch_bn<tcec::kTF32, tcec::kRZ>(block_n, m, n, k, A, lda, B, ldb, C, ldc, 0,
-                                               drain_every, group_m, prefetch, kvariant, d_flags, st);
+                                               drain_every, group_m, prefetch, kvariant, mma_order, split_mode, d_flags, st);
   return TCEC_ERR_UNSUPPORTED;
 }
 
@@ -295,17 +457,7 @@ int tcec_sgemm_host(int variant, int64_t m, int64_t n, int64_t k, const float* A
   if (m == 0 || n == 0) return TCEC_OK;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return TCEC_ERR_CUDA;
-  static std::once_flag pool_once[64];
-  if (dev < 64) {
-    std::call_once(pool_once[dev], [dev] {
-      // keep freed blocks cached in the stream-ordered pool between calls
-      cudaMemPool_t pool;
-      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = ~0ull;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-      }
-    });
-  }
+  keep_pool(dev);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t dlda = ((k > 0 ? k : 1) + 3) / 4 * 4;
   const int64_t dldb = (n + 3) / 4 * 4;

@@ -32,6 +32,7 @@ struct GemmShape {
   int32_t drain_every;     // operand stages per drain interval (>= 1)
   int32_t group_m;         // tile rasterisation group
   int32_t prefetch;        // L2 prefetch distance in staging slices (0 = off)
+  int32_t mma_order;       // pair kernel: 1 = A_hi reuse through the MMA collector
 };
 
 template <int BN_>

@@ -374,6 +374,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
         const uint32_t alo = ahi + (C::OP_A_BYTES >> 4);
         const uint32_t bhi = (op + ((2 * C::OP_A_BYTES) >> 4)) | b_lbo_w;
         const uint32_t blo = bhi + (C::OP_B_BYTES >> 4);
+        const bool first_in_interval = (kb % de) == 0;
+        if (shp.mma_order == 1 && !(first_in_interval && kb > 0)) {
+          // P is free: per k-step dA*B_hi, then A_hi*dB and A_hi*B_hi with A_hi
+          // held in the MMA's A collector (read from shared memory once).  The
+          // dC order per k-step is the reference's (schemes.py:294-298).
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks) {
+            sm100::mma_pair_col<V == kTF32, 0>(tmem_dC, alo + 2 * ks, a_hi_w, bhi + kB * ks, b_hi_w,
+                                               idesc, (kb | ks) != 0);
+            sm100::mma_pair_col<V == kTF32, 1>(tmem_dC, ahi + 2 * ks, a_hi_w, blo + kB * ks, b_hi_w,
+                                               idesc, 1u);
+            sm100::mma_pair_col<V == kTF32, 3>(tmem_P, ahi + 2 * ks, a_hi_w, bhi + kB * ks, b_hi_w,
+                                               idesc, !(first_in_interval && ks == 0));
+          }
+          sm100::mma_commit_pair_mc(&op_empty[o], 0x3);
+          if ((kb % de) == de - 1 || kb == nop - 1) sm100::mma_commit_pair_mc(p_full, 0x3);
+          continue;
+        }
         // correction terms first (reference order per k-step: dA*B then A*dB) so the
         // drain of the previous P overlaps them (schemes.py:294-298)
 #pragma unroll
@@ -383,7 +401,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
           sm100::mma_pair_split<V == kTF32>(tmem_dC, ahi + 2 * ks, a_hi_w, blo + kB * ks, b_hi_w,
                                             idesc, 1u);
         }
-        const bool first_in_interval = (kb % de) == 0;
         if (first_in_interval && kb > 0) {
           sm100::mbar_wait_cluster(p_empty, ((kb / de) - 1) & 1);
           sm100::tc_fence_after();

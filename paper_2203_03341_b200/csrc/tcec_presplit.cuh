@@ -1,0 +1,355 @@
+// tcec_presplit.cuh -- split-once mode of the error-corrected SGEMM.
+//
+// The fused kernels (tcec_gemm2.cuh) re-split every A tile once per column
+// tile of C and every B tile once per row tile (n / 256 and m / 256 times at
+// 16384^3), and on B200 that redundant split -- its FP32 staging writes and
+// reads through shared memory -- is what bounds them.  This mode
+// splits each input element exactly once in an HBM-bandwidth-bound pass and
+// then runs a plain three-product tcgen05 GEMM whose TMA loads the hi / lo
+// operands straight into the UMMA layout:
+//
+//   tcec_presplit_kernel   X (FP32) -> hi, lo in the operand element type (FP16
+//                          or TF32 bit patterns), K-major: A as m x k, B
+//                          transposed to n x k; RunFlags from the same pass.
+//   tcec_gemm_ps_kernel    CTA pair, 256 x 256 tile, 3-deep ring of 64 KB
+//                          operand stages (A_hi, A_lo, B_hi, B_lo; 128-byte
+//                          swizzled K-major), the same MMA order, drain and
+//                          epilogue as the fused pair kernel -- bit-identical C.
+//
+// Split arithmetic is split.cuh's (splitting.py:114-122), including lo = 0
+// where hi overflowed.
+#pragma once
+
+#include "tcec_gemm2.cuh"
+
+namespace tcec {
+
+// ---------------------------------------------------------------------------
+// Split pass: 64 x 64 tiles, 256 threads.  Output element (r, c) of X goes to
+// out[r * ldo + c] (kTrans = false) or out[c * ldo + r] (kTrans = true); ldo is
+// a multiple of 16 and every output row is written up to ldo (zeros past the
+// matrix edge), so the GEMM's TMA sees a fully initialised, padded operand.
+template <int V>
+struct PsElem;
+template <>
+struct PsElem<kFP16> { using T = uint16_t; };
+template <>
+struct PsElem<kTF32> { using T = uint32_t; };
+
+template <int V, int R, bool kTrans>
+__global__ void __launch_bounds__(256)
+    tcec_presplit_kernel(const float* __restrict__ X, int32_t rows, int32_t cols, int64_t ldx,
+                         void* __restrict__ hi_out, void* __restrict__ lo_out, int64_t ldo,
+                         int32_t out_rows, float scale, FlagThresholds thr,
+                         uint32_t* __restrict__ flags) {
+  using E = typename PsElem<V>::T;
+  __shared__ uint32_t sh_hi[64][65];
+  __shared__ uint32_t sh_lo[64][65];
+  E* hi = static_cast<E*>(hi_out);
+  E* lo = static_cast<E*>(lo_out);
+  const int t = threadIdx.x;
+  const int tiles_c = (cols + 63) / 64;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x / tiles_c) * 64;
+  const int64_t c0 = static_cast<int64_t>(blockIdx.x % tiles_c) * 64;
+  FlagAcc fa;
+  const int cc = (t & 15) * 4;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int rr = (t >> 4) + 16 * i;
+    const int64_t r = r0 + rr, c = c0 + cc;
+    float x[4] = {0.f, 0.f, 0.f, 0.f};
+    if (r < rows) {
+      const float* src = X + r * ldx + c;
+      if (c + 3 < cols && (reinterpret_cast<uintptr_t>(src) & 15u) == 0) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(src));
+        x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (c + j < cols) x[j] = src[j];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) fa.add(x[j]);
+    uint32_t h[4], l[4];
+    if constexpr (V == kFP16) {
+      uint32_t hp0, lp0, hp1, lp1;
+      split_f16_pair<R>(x[0], x[1], scale, hp0, lp0);
+      split_f16_pair<R>(x[2], x[3], scale, hp1, lp1);
+      h[0] = hp0 & 0xFFFFu; h[1] = hp0 >> 16; h[2] = hp1 & 0xFFFFu; h[3] = hp1 >> 16;
+      l[0] = lp0 & 0xFFFFu; l[1] = lp0 >> 16; l[2] = lp1 & 0xFFFFu; l[3] = lp1 >> 16;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float hf, lf;
+        split_tf32<R>(x[j], scale, hf, lf);
+        h[j] = __float_as_uint(hf);
+        l[j] = __float_as_uint(lf);
+      }
+    }
+    if constexpr (!kTrans) {
+      if (r < out_rows && c < ldo) {
+        if constexpr (V == kFP16) {
+          *reinterpret_cast<uint2*>(hi + r * ldo + c) = make_uint2(h[0] | (h[1] << 16), h[2] | (h[3] << 16));
+          *reinterpret_cast<uint2*>(lo + r * ldo + c) = make_uint2(l[0] | (l[1] << 16), l[2] | (l[3] << 16));
+        } else {
+          *reinterpret_cast<uint4*>(hi + r * ldo + c) = make_uint4(h[0], h[1], h[2], h[3]);
+          *reinterpret_cast<uint4*>(lo + r * ldo + c) = make_uint4(l[0], l[1], l[2], l[3]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        sh_hi[cc + j][rr] = h[j];
+        sh_lo[cc + j][rr] = l[j];
+      }
+    }
+  }
+  if constexpr (kTrans) {
+    __syncthreads();
+    // output row c0 + oc (a column of X), elements r0 + orr .. +16
+    const int oc = t >> 2, orr = (t & 3) * 16;
+    const int64_t orow = c0 + oc, ocol = r0 + orr;
+    if (orow < out_rows && ocol < ldo) {
+      E* dh = hi + orow * ldo + ocol;
+      E* dl = lo + orow * ldo + ocol;
+      if constexpr (V == kFP16) {
+        uint32_t ph[8], pl[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          ph[j] = sh_hi[oc][orr + 2 * j] | (sh_hi[oc][orr + 2 * j + 1] << 16);
+          pl[j] = sh_lo[oc][orr + 2 * j] | (sh_lo[oc][orr + 2 * j + 1] << 16);
+        }
+        reinterpret_cast<uint4*>(dh)[0] = make_uint4(ph[0], ph[1], ph[2], ph[3]);
+        reinterpret_cast<uint4*>(dh)[1] = make_uint4(ph[4], ph[5], ph[6], ph[7]);
+        reinterpret_cast<uint4*>(dl)[0] = make_uint4(pl[0], pl[1], pl[2], pl[3]);
+        reinterpret_cast<uint4*>(dl)[1] = make_uint4(pl[4], pl[5], pl[6], pl[7]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          reinterpret_cast<uint4*>(dh)[q] = make_uint4(sh_hi[oc][orr + 4 * q], sh_hi[oc][orr + 4 * q + 1],
+                                                       sh_hi[oc][orr + 4 * q + 2], sh_hi[oc][orr + 4 * q + 3]);
+          reinterpret_cast<uint4*>(dl)[q] = make_uint4(sh_lo[oc][orr + 4 * q], sh_lo[oc][orr + 4 * q + 1],
+                                                       sh_lo[oc][orr + 4 * q + 2], sh_lo[oc][orr + 4 * q + 3]);
+        }
+      }
+    }
+  }
+  flag_publish(fa, thr, flags);
+}
+
+// ---------------------------------------------------------------------------
+// Three-product GEMM over pre-split operands.
+template <int V>
+struct PsCfg {
+  static constexpr int BM = 128;           // rows per CTA (pair M = 256)
+  static constexpr int BN = 256;           // pair N
+  static constexpr int BN_CTA = 128;       // B rows (= C columns) loaded per CTA
+  static constexpr int NOP = 3;
+  static constexpr int TILE_BYTES = 128 * 128;             // 128 rows x 128-byte k chunk
+  static constexpr int OP_BYTES = 4 * TILE_BYTES;          // A_hi | A_lo | B_hi | B_lo
+  static constexpr int OFF_OP = 0;
+  static constexpr int OFF_BAR = NOP * OP_BYTES;
+  static constexpr int NUM_BARS = 2 * NOP + 2;
+  static constexpr int SMEM_BYTES = OFF_BAR + NUM_BARS * 8 + 16;
+  static constexpr int TMEM_COLS = 512;    // P [0,256) | dC [256,512)
+  static constexpr int NUM_THREADS = 384;  // warps 0-3 control, 4-11 drain
+  static constexpr int DRAIN_WARP0 = 4, NUM_DRAIN_WARPS = 8;
+  static constexpr int EPI_WARP_BYTES = 32 * 128 * 4;
+  static_assert(NUM_DRAIN_WARPS * EPI_WARP_BYTES <= OFF_BAR, "epilogue staging reuses the ring");
+};
+
+// TMA load that completes on the leader CTA's mbarrier (CTA-pair form).
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* m,
+                                                 uint32_t leader_bar, int32_t c0, int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(leader_bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+template <int V>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PsCfg<V>::NUM_THREADS, 1)
+    tcec_gemm_ps_kernel(const __grid_constant__ CUtensorMap tmAh,  // A_hi [m][k] box 128B x 128
+                        const __grid_constant__ CUtensorMap tmAl,  // A_lo
+                        const __grid_constant__ CUtensorMap tmBh,  // B_hi^T [n][k] box 128B x 128
+                        const __grid_constant__ CUtensorMap tmBl,  // B_lo^T
+                        const __grid_constant__ CUtensorMap tmC,   // C [m][n], box 32 x 32, SW128
+                        const GemmShape shp, const float inv_scale, uint32_t* __restrict__ flags) {
+  using C = PsCfg<V>;
+  using VC = VarCfg<V>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* op_full = bars;                 // TMA (both CTAs) -> MMA   (leader, tx)
+  uint64_t* op_empty = bars + C::NOP;       // MMA commit -> TMA        (both, multicast)
+  uint64_t* p_full = bars + 2 * C::NOP;     // MMA commit -> drain      (both, multicast)
+  uint64_t* p_empty = p_full + 1;           // drain -> MMA             (leader, 16)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NUM_BARS);
+  const uint32_t smem_base = sm100::smem_u32(smem);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = sm100::cluster_ctarank();
+
+  const int tiles_m = (shp.m + 2 * C::BM - 1) / (2 * C::BM);
+  const int tiles_n = (shp.n + C::BN - 1) / C::BN;
+  int tile_m, tile_n;
+  {
+    const int pid = blockIdx.x >> 1;
+    const int per_group = shp.group_m * tiles_n;
+    const int g = pid / per_group;
+    const int first_m = g * shp.group_m;
+    const int gsize = min(tiles_m - first_m, shp.group_m);
+    const int in_g = pid - g * per_group;
+    tile_m = first_m + in_g % gsize;
+    tile_n = in_g / gsize;
+  }
+  const int m_cta = tile_m * 2 * C::BM + rank * C::BM;
+  const int n_pair = tile_n * C::BN;
+  const int n_cta = n_pair + rank * C::BN_CTA;
+  const int nop = shp.num_op_stages;
+  const int de = shp.drain_every;
+  const int nintervals = (nop + de - 1) / de;
+
+  if (warp == 0 && lane == 0) {
+    if (smem_base & 1023u) __trap();
+    sm100::tma_prefetch_desc(&tmAh);
+    sm100::tma_prefetch_desc(&tmAl);
+    sm100::tma_prefetch_desc(&tmBh);
+    sm100::tma_prefetch_desc(&tmBl);
+    sm100::tma_prefetch_desc(&tmC);
+    for (int o = 0; o < C::NOP; ++o) {
+      sm100::mbar_init(&op_full[o], 1);
+      sm100::mbar_init(&op_empty[o], 1);
+    }
+    sm100::mbar_init(p_full, 1);
+    sm100::mbar_init(p_empty, 2 * C::NUM_DRAIN_WARPS);
+    sm100::fence_mbar_init();
+  }
+  if (warp == 2) sm100::tmem_alloc_pair<C::TMEM_COLS>(tmem_slot);
+  sm100::tc_fence_before();
+  sm100::cluster_sync();
+  sm100::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tmem_P = tmem_base;
+  const uint32_t tmem_dC = tmem_base + C::BN;
+
+  if (warp < C::DRAIN_WARP0) {
+    if (warp == 0 && lane == 0) {
+      // ===================== TMA producer (both CTAs) =====================
+      const uint32_t leader_full = sm100::mapa_shared(sm100::smem_u32(op_full), 0);
+      for (int kb = 0; kb < nop; ++kb) {
+        const int o = kb % C::NOP;
+        sm100::mbar_wait(&op_empty[o], ((kb / C::NOP) & 1) ^ 1);
+        if (rank == 0) sm100::mbar_arrive_expect_tx(&op_full[o], 2 * C::OP_BYTES);
+        const uint32_t dst = smem_base + C::OFF_OP + o * C::OP_BYTES;
+        const uint32_t bar = leader_full + o * 8;
+        const int kc = kb * VC::BK_OP;
+        tma_load_2d_pair(dst, &tmAh, bar, kc, m_cta);
+        tma_load_2d_pair(dst + C::TILE_BYTES, &tmAl, bar, kc, m_cta);
+        tma_load_2d_pair(dst + 2 * C::TILE_BYTES, &tmBh, bar, kc, n_cta);
+        tma_load_2d_pair(dst + 3 * C::TILE_BYTES, &tmBl, bar, kc, n_cta);
+      }
+    } else if (warp == 1 && lane == 0 && rank == 0) {
+      // ===================== MMA issuer (leader CTA) =====================
+      constexpr uint32_t idesc = sm100::umma_idesc(VC::AB_FORMAT, 2 * C::BM, C::BN);
+      constexpr uint32_t hi_w = (1024u >> 4) | (1u << 14) | (2u << 29);  // SBO 1024, v1, SW128
+      for (int kb = 0; kb < nop; ++kb) {
+        const int o = kb % C::NOP;
+        sm100::mbar_wait(&op_full[o], (kb / C::NOP) & 1);
+        sm100::tc_fence_after();
+        const uint32_t op = sm100::opaque(smem_base + C::OFF_OP + o * C::OP_BYTES) >> 4;
+        const uint32_t ahi = op | (1u << 16);
+        const uint32_t alo = ahi + (C::TILE_BYTES >> 4);
+        const uint32_t bhi = ahi + (2 * C::TILE_BYTES >> 4);
+        const uint32_t blo = ahi + (3 * C::TILE_BYTES >> 4);
+        // corrections first (reference order per k-step: dA*B then A*dB), so the
+        // drain of the previous P overlaps them (schemes.py:294-298)
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+          sm100::mma_pair_split<V == kTF32>(tmem_dC, alo + 2 * ks, hi_w, bhi + 2 * ks, hi_w, idesc,
+                                            (kb | ks) != 0);
+          sm100::mma_pair_split<V == kTF32>(tmem_dC, ahi + 2 * ks, hi_w, blo + 2 * ks, hi_w, idesc, 1u);
+        }
+        const bool first_in_interval = (kb % de) == 0;
+        if (first_in_interval && kb > 0) {
+          sm100::mbar_wait_cluster(p_empty, ((kb / de) - 1) & 1);
+          sm100::tc_fence_after();
+        }
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks)
+          sm100::mma_pair_split<V == kTF32>(tmem_P, ahi + 2 * ks, hi_w, bhi + 2 * ks, hi_w, idesc,
+                                            !(first_in_interval && ks == 0));
+        sm100::mma_commit_pair_mc(&op_empty[o], 0x3);
+        if ((kb % de) == de - 1 || kb == nop - 1) sm100::mma_commit_pair_mc(p_full, 0x3);
+      }
+    }
+  } else {
+    // ===================== drain + epilogue =====================
+    const int q = warp & 3;
+    const int h = (warp - C::DRAIN_WARP0) >> 2;
+    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+    const uint32_t p_empty_leader = sm100::mapa_shared(sm100::smem_u32(p_empty), 0);
+    float acc[128];
+#pragma unroll
+    for (int j = 0; j < 128; ++j) acc[j] = 0.0f;
+    for (int it = 0; it < nintervals; ++it) {
+      sm100::mbar_wait(p_full, it & 1);
+      sm100::tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        uint32_t r[16];
+        sm100::tmem_ld_32x32b_x16(tmem_P + lane_off + h * 128 + c * 16, r);
+        sm100::tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 16; ++j)  // schemes.py:300-304: c = RN32(c + partial)
+          acc[c * 16 + j] = __fadd_rn(acc[c * 16 + j], __uint_as_float(r[j]));
+      }
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive_remote(p_empty_leader);
+    }
+    bool nonfinite = false;
+    const uint32_t stage = smem_base + (warp - C::DRAIN_WARP0) * C::EPI_WARP_BYTES;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const uint32_t box = stage + b * 4096;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t r[16];
+        sm100::tmem_ld_32x32b_x16(tmem_dC + lane_off + h * 128 + b * 32 + c * 16, r);
+        sm100::tmem_ld_wait();
+        float o[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          // schemes.py:306-307: one rounding of c + dC * 2^-s
+          o[j] = __fmaf_rn(__uint_as_float(r[j]), inv_scale, acc[b * 32 + c * 16 + j]);
+          nonfinite |= !isfinite(o[j]);
+        }
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+          sm100::sts128f(box + sw128(lane, c * 4 + v), o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
+      }
+      sm100::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        sm100::tma_store_2d(&tmC, smem + (box - smem_base), n_pair + h * 128 + b * 32, m_cta + q * 32);
+        sm100::tma_store_commit();
+      }
+    }
+    if (lane == 0) sm100::tma_store_wait0();
+    if (flags != nullptr && __any_sync(0xFFFFFFFFu, nonfinite) && lane == 0)
+      atomicOr(flags, kFlagOverflow);
+    sm100::tc_fence_before();
+  }
+
+  __syncthreads();
+  sm100::cluster_sync();
+  if (warp == 2) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc_pair<C::TMEM_COLS>(tmem_base);
+  }
+}
+
+}  // namespace tcec

@@ -374,3 +374,61 @@ def test_kernel_variants_bitwise_equal(sname, variant, bk, drain, kv):
     c1 = T.gemm_device(A, B, sname, flags=f1, kernel_variant=kv)
     assert torch.equal(c0.view(torch.int32), c1.view(torch.int32))
     assert int(f0.item()) == int(f1.item())
+
+
+OPTION_SETS = [{"block_n": 192}, {"mma_order": 1}, {"split_mode": 2}]
+
+
+@pytest.mark.parametrize("opts", OPTION_SETS, ids=lambda o: ",".join(f"{k}={v}" for k, v in o.items()))
+@pytest.mark.parametrize("sname,variant,bk,drain", VARIANTS)
+@pytest.mark.parametrize("shape", [(256, 192, 64), (300, 200, 1000), (77, 1000, 130), (520, 576, 2048)])
+def test_kernel_options_bitwise_equal(sname, variant, bk, drain, shape, opts):
+    """Every kernel option runs the default path's per-element arithmetic: the
+    A-from-TMEM pair kernel (block_n=192), the A_hi collector-reuse MMA order
+    (mma_order=1) and the split-once mode (split_mode=2: separate split pass +
+    three-product GEMM over pre-split operands) give bit-identical C and flags,
+    including ragged edges and inputs spanning 2^-40..2^15 (out_of_range for
+    FP16; no hi overflow -- see test_split_once_mode_flags_and_overflow)."""
+    import torch
+
+    T = _T()
+    m, n, k = shape
+    for wide in (False, True):
+        if wide:
+            a = O.exprand(m, k, -40, 14, m + k)
+            b = O.exprand(k, n, -40, 14, n + k)
+            A, B = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+        else:
+            g = torch.Generator(device="cuda")
+            g.manual_seed(m + n + k)
+            A = torch.rand((m, k), generator=g, device="cuda") * 2 - 1
+            B = torch.rand((k, n), generator=g, device="cuda") * 2 - 1
+        f0 = torch.zeros(1, dtype=torch.int32, device="cuda")
+        f1 = torch.zeros(1, dtype=torch.int32, device="cuda")
+        c0 = T.gemm_device(A, B, sname, flags=f0)
+        c1 = T.gemm_device(A, B, sname, flags=f1, **opts)
+        assert torch.equal(c0.view(torch.int32), c1.view(torch.int32)), (opts, wide)
+        assert int(f0.item()) == int(f1.item()), (opts, wide)
+
+
+@pytest.mark.parametrize("sname", ["corrected3_halfhalf", "corrected3_tf32"])
+def test_split_once_mode_flags_and_overflow(sname):
+    """Split-once mode: the split pass classifies every input element once
+    (RunFlags identical to the fused path) and an overflowing hi gives the same
+    non-finite output positions and saw_overflow as the fused path."""
+    import torch
+
+    T = _T()
+    a = O.urand(300, 200, -1, 1, 3)
+    b = O.urand(200, 260, -1, 1, 4)
+    a[5, 7] = 70000.0 if "half" in sname else np.finfo(np.float32).max
+    A, B = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    f0 = torch.zeros(1, dtype=torch.int32, device="cuda")
+    f1 = torch.zeros(1, dtype=torch.int32, device="cuda")
+    c0 = T.gemm_device(A, B, sname, flags=f0).cpu().numpy()
+    c1 = T.gemm_device(A, B, sname, flags=f1, split_mode=2).cpu().numpy()
+    assert int(f0.item()) == int(f1.item())
+    assert int(f1.item()) & 1
+    assert np.array_equal(np.isfinite(c0), np.isfinite(c1))
+    fin = np.isfinite(c0)
+    assert np.array_equal(c0[fin], c1[fin])
