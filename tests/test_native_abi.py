@@ -44,8 +44,14 @@ def test_version_and_status_strings(lib):
 
 
 def test_opts_struct_matches_header():
-    # int32 x 5 + int32[3]
-    assert ctypes.sizeof(N.TcecOpts) == 32
+    """The ctypes mirror lists exactly the header's tcec_opts fields, in order."""
+    hdr = open(HEADER).read()
+    body = hdr.split("typedef struct tcec_opts {")[1].split("} tcec_opts;")[0]
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    fields = re.findall(r"int32_t\s+(\w+)(?:\[(\d+)\])?;", body)
+    assert [(name, int(cnt or 1)) for name, cnt in fields] == \
+        [(name, getattr(typ, "_length_", 1)) for name, typ in N.TcecOpts._fields_]
+    assert ctypes.sizeof(N.TcecOpts) == 4 * sum(int(cnt or 1) for _, cnt in fields)
 
 
 def test_argument_validation_without_gpu(lib):
