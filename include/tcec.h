@@ -35,6 +35,21 @@ extern "C" {
 #define TCEC_FLAG_OUT_OF_RANGE 2u /* some input outside the split's representable band */
 #define TCEC_FLAG_NONFINITE_INPUT 4u /* some input is inf or NaN (the reference raises) */
 
+/* Product schedules (tcec_opts.scheme).  CORRECTED3 is the accelerated path;
+ * the others run the reference's comparator schemes on the tensor core so the
+ * paper's ablations can be reproduced on hardware (they use split-once mode):
+ *   CORRECTED3_DD  corrected3 plus the dA*dB chain in a separate accumulator
+ *                  (schemes.py:308-313, delta_term_ablation :422-451)
+ *   TC_PLAIN       tc_plain_fp16 / tc_plain_tf32: one product of the inputs
+ *                  converted RN (FP16) / RNA (TF32) (schemes.py:343-351)
+ *   INUNIT4        markidis4 / corrected4 with the hardware's terminal
+ *                  rounding: four products in one accumulator, unscaled split
+ *                  (schemes.py:99-117, :352-364)  */
+#define TCEC_SCHEME_CORRECTED3 0
+#define TCEC_SCHEME_CORRECTED3_DD 1
+#define TCEC_SCHEME_TC_PLAIN 2
+#define TCEC_SCHEME_INUNIT4 3
+
 /* Status codes. */
 #define TCEC_OK 0
 #define TCEC_ERR_ARG (-1)         /* bad shape / leading dimension / option      */
@@ -63,6 +78,8 @@ typedef struct tcec_opts {
    * pre-split operands (workspace 2(m + n)k operand elements, stream-ordered
    * allocation).  Results are bit-identical. */
   int32_t split_mode;
+  /* Product schedule, TCEC_SCHEME_* (0 = corrected3). */
+  int32_t scheme;
   /* reserved[0]: L2 prefetch distance in 32-deep k-slices (0 = off);
    * reserved[1]: pair-kernel variant (0 = split + drain warps, 1 = unified workers);
    * reserved[2]: pair-kernel MMA order (0 = corrections first, 1 = A_hi collector reuse). */

@@ -55,6 +55,9 @@ def lib():
             i32, i32, i32, i64, i64, i64, p, i64, p, i64, p, i64,
             i32, i32, i32, i32, i32, p,
         ]
+        L.tcec_oracle_inunit.argtypes = [
+            i32, i32, i32, i32, i32, i64, i64, i64, p, i64, p, i64, p, i64, i32, i32, p,
+        ]
         L.tcec_oracle_fp32_simt.argtypes = [i64, i64, i64, p, i64, p, i64, p, i64, i32]
         L.tcec_oracle_fp64_ref.argtypes = [i64, i64, i64, p, i64, p, i64, p, i64]
         _lib = L
@@ -111,6 +114,29 @@ def corrected3(a, b, variant: str = "fp16", block_k: int = 16, drain_k: int | No
         fmt, s, rm, m, n, k, _ptr(a), k, _ptr(b), n, _ptr(c), n,
         block_k, drain_k or block_k, acc_bits, int(include_dd), nthreads,
         ctypes.byref(flags))
+    if rc != 0:
+        raise ValueError(f"oracle rejected arguments (rc={rc})")
+    return c, int(flags.value)
+
+
+def inunit(a, b, scheme: str, block_k: int = 16, acc_bits: int = 25):
+    """schemes.py:gemm for the in-unit comparators restated (tcec_oracle_inunit):
+    scheme in tc_plain_fp16, tc_plain_tf32, markidis4, markidis4_tf32,
+    corrected4_rn, corrected4_rz.  Returns (C float32, flags int)."""
+    kinds = {"tc_plain_fp16": (0, 0, 0, 0, 2), "tc_plain_tf32": (0, 1, 0, 1, 2),
+             "markidis4": (1, 0, 0, 0, 2), "markidis4_tf32": (1, 1, 0, 1, 2),
+             "corrected4_rn": (1, 0, 0, 0, 0), "corrected4_rz": (1, 0, 0, 0, 2)}
+    kind, fmt, s, rm, term = kinds[scheme]
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    b = np.ascontiguousarray(b, dtype=np.float32)
+    m, k = a.shape
+    k2, n = b.shape
+    if k2 != k:
+        raise ValueError(f"inner dimensions differ: {k} vs {k2}")
+    c = np.empty((m, n), np.float32)
+    flags = ctypes.c_uint32(0)
+    rc = lib().tcec_oracle_inunit(kind, fmt, s, rm, term, m, n, k, _ptr(a), k, _ptr(b), n,
+                                  _ptr(c), n, block_k, acc_bits, ctypes.byref(flags))
     if rc != 0:
         raise ValueError(f"oracle rejected arguments (rc={rc})")
     return c, int(flags.value)

@@ -366,3 +366,89 @@ int tcec_oracle_fp64_ref(int64_t m, int64_t n, int64_t k, const float *A, int64_
     }
   return 0;
 }
+
+/* In-unit comparator schemes, schemes.py:343-364 (gemm's TC_PLAIN and
+ * MARKIDIS4 / CORRECTED4 branches), single-threaded (test sizes only).
+ *   kind 0, tc_plain:  A, B converted round_to_format(., f, mode)
+ *                      (schemes.py:345-348), one term, flags from
+ *                      _plain_conversion_flags (:227-232)
+ *   kind 1, four-term: split (f, s, mode) (:353-356), terms per block in the
+ *                      reference's order dA*dB, dA*B, A*dB, A*B (:361-363)
+ *                      through one accumulator (_run_in_unit_terms :250-262)
+ * Per block every term's 25-bit RZ block sum (mma.py:65-81) enters C with the
+ * terminal rounding `term_mode` (mma.py:84-85: RZ for tc_plain / markidis4, the
+ * scheme's terminal for corrected4).  Output cast to FP32, non-finite output
+ * raises the overflow flag (:369-371). */
+int tcec_oracle_inunit(int kind, int f, int s, int mode, int term_mode, int64_t m, int64_t n,
+                       int64_t k, const float *A, int64_t lda, const float *B, int64_t ldb,
+                       float *C, int64_t ldc, int block_k, int acc_bits, uint32_t *flags) {
+  if (m < 0 || n < 0 || k < 0 || block_k < 1 || acc_bits < 1 || acc_bits > 53) return -1;
+  if (kind != 0 && kind != 1) return -1;
+  const int64_t kp = ((k + block_k - 1) / block_k) * block_k;
+  double *ah = calloc((size_t)(m * kp + 1), sizeof(double));
+  double *al = calloc((size_t)(m * kp + 1), sizeof(double));
+  double *bh = calloc((size_t)(n * kp + 1), sizeof(double));
+  double *bl = calloc((size_t)(n * kp + 1), sizeof(double));
+  if (!ah || !al || !bh || !bl) {
+    free(ah); free(al); free(bh); free(bl);
+    return -2;
+  }
+  uint32_t fl = 0;
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t t = 0; t < k; ++t) {
+      const double x = (double)A[i * lda + t];
+      if (kind == 0) {
+        const double c = round_to_format(x, f, mode);
+        ah[i * kp + t] = c;
+        if (isinf(c)) fl |= ORACLE_FLAG_OVERFLOW | ORACLE_FLAG_OUT_OF_RANGE;
+        if (c == 0.0 && x != 0.0) fl |= ORACLE_FLAG_OUT_OF_RANGE;
+      } else {
+        split_one(x, f, s, mode, &ah[i * kp + t], &al[i * kp + t]);
+        if (isinf(ah[i * kp + t])) fl |= ORACLE_FLAG_OVERFLOW;
+        if (classify_one(x, f, s) == 2) fl |= ORACLE_FLAG_OUT_OF_RANGE;
+      }
+    }
+  for (int64_t t = 0; t < k; ++t)
+    for (int64_t j = 0; j < n; ++j) {
+      const double x = (double)B[t * ldb + j];
+      if (kind == 0) {
+        const double c = round_to_format(x, f, mode);
+        bh[j * kp + t] = c;
+        if (isinf(c)) fl |= ORACLE_FLAG_OVERFLOW | ORACLE_FLAG_OUT_OF_RANGE;
+        if (c == 0.0 && x != 0.0) fl |= ORACLE_FLAG_OUT_OF_RANGE;
+      } else {
+        split_one(x, f, s, mode, &bh[j * kp + t], &bl[j * kp + t]);
+        if (isinf(bh[j * kp + t])) fl |= ORACLE_FLAG_OVERFLOW;
+        if (classify_one(x, f, s) == 2) fl |= ORACLE_FLAG_OUT_OF_RANGE;
+      }
+    }
+  const int64_t nb = kp / block_k;
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t j = 0; j < n; ++j) {
+      const double *ta[4], *tb[4];
+      int nt;
+      if (kind == 0) {
+        ta[0] = ah + i * kp; tb[0] = bh + j * kp; nt = 1;
+      } else {
+        ta[0] = al + i * kp; tb[0] = bl + j * kp;
+        ta[1] = al + i * kp; tb[1] = bh + j * kp;
+        ta[2] = ah + i * kp; tb[2] = bl + j * kp;
+        ta[3] = ah + i * kp; tb[3] = bh + j * kp;
+        nt = 4;
+      }
+      double c = 0.0;
+      for (int64_t b = 0; b < nb; ++b)
+        for (int u = 0; u < nt; ++u) {
+          double acc = 0.0;
+          for (int64_t t = b * block_k; t < (b + 1) * block_k; ++t)
+            acc = truncate_raw(sum_round_to_odd(acc, ta[u][t] * tb[u][t]), acc_bits);
+          c = round_to_format(sum_round_to_odd(acc, c), FMT_FP32, term_mode);
+        }
+      const float cf = (float)c;
+      if (!isfinite(cf)) fl |= ORACLE_FLAG_OVERFLOW;
+      C[i * ldc + j] = cf;
+    }
+  free(ah); free(al); free(bh); free(bl);
+  if (flags) *flags = fl;
+  return 0;
+}

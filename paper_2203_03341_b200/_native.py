@@ -41,6 +41,7 @@ class TcecOpts(ctypes.Structure):
         ("block_n", ctypes.c_int32),
         ("group_m", ctypes.c_int32),
         ("split_mode", ctypes.c_int32),
+        ("scheme", ctypes.c_int32),
         ("reserved", ctypes.c_int32 * 3),
     ]
 
@@ -100,9 +101,11 @@ def check(status: int, what: str) -> None:
 
 def make_opts(split_rounding: int = ROUND_DEFAULT, scale_log2: int = -1, drain_k: int = 0,
               block_n: int = 0, group_m: int = 0, prefetch: int = 0,
-              kernel_variant: int = 0, mma_order: int = 0, split_mode: int = 0) -> TcecOpts:
+              kernel_variant: int = 0, mma_order: int = 0, split_mode: int = 0,
+              scheme: int = 0) -> TcecOpts:
     o = TcecOpts()
     o.split_mode = split_mode
+    o.scheme = scheme
     o.reserved[0] = prefetch
     o.reserved[1] = kernel_variant
     o.reserved[2] = mma_order

@@ -153,6 +153,27 @@ __host__ __device__ inline FlagThresholds flag_thresholds(int variant, int round
   return t;
 }
 
+// RunFlags of a plain conversion (schemes.py:227-232, _plain_conversion_flags):
+// overflow = some converted value is inf; out_of_range = overflow or some
+// nonzero x converts to 0.  FP16 RN: x vanishes iff |x| <= 2^-25 (the tie
+// rounds to even zero); TF32 RNA: iff |x| < 2^-137 (the tie rounds away).
+__host__ __device__ inline FlagThresholds plain_thresholds(int variant, int rounding) {
+  FlagThresholds t;
+  const float inf = bits_to_float(0x7F800000u);
+  if (variant == kFP16) {
+    const uint32_t first_kept = ((static_cast<uint32_t>(-25 + 127) << 23) + 1u);  // next above 2^-25
+    t.tiny2 = rounding == kRZ ? ((static_cast<uint32_t>(-24 + 127) << 23) * 2u - 2u)
+                              : first_kept * 2u - 2u;
+    t.ovf = (rounding == kRZ) ? inf : 65520.0f;
+  } else {
+    const uint32_t first_kept = rounding == kRZ ? 0x2000u : (rounding == kRNA ? 0x1000u : 0x1001u);
+    t.tiny2 = first_kept * 2u - 2u;
+    t.ovf = (rounding == kRZ) ? inf : bits_to_float(0x7F7FF000u);
+  }
+  t.big = t.ovf;  // an overflowing conversion is also out of range
+  return t;
+}
+
 __device__ __forceinline__ uint32_t flag_bits(const FlagAcc& f, const FlagThresholds& t) {
   uint32_t fl = 0;
   if (!(f.mx <= 3.402823466e38f)) return kFlagNonfiniteInput;  // inf or NaN input

@@ -224,11 +224,11 @@ int launch_gemm_ts(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda,
 
 // Split-once mode: one split pass per input (A as m x k, B transposed to
 // n x k, both K-major in the operand type), then the three-product GEMM.
-template <int V, int R>
+template <int V, int R, int S>
 int launch_gemm_presplit(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda,
                          const float* B, int64_t ldb, float* C, int64_t ldc, int scale_log2,
                          int drain_every, int group_m, uint32_t* d_flags, cudaStream_t stream) {
-  using Cfg = tcec::PsCfg<V>;
+  using Cfg = tcec::PsCfg<V, S>;
   using VC = tcec::VarCfg<V>;
   const uint32_t esize = V == tcec::kFP16 ? 2u : 4u;
   const CUtensorMapDataType dt =
@@ -252,7 +252,7 @@ int launch_gemm_presplit(int64_t m, int64_t n, int64_t k, const float* A, int64_
   if (!st) st = make_tmap_op(&tmBh, bh, dt, esize, k, n, ldk, Cfg::BN_CTA);
   if (!st) st = make_tmap_op(&tmBl, bl, dt, esize, k, n, ldk, Cfg::BN_CTA);
   if (!st) st = make_tmap(&tmC, C, n, m, ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
-  auto kern = tcec::tcec_gemm_ps_kernel<V>;
+  auto kern = tcec::tcec_gemm_ps_kernel<V, S>;
   static std::once_flag attr_once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(attr_once, [&] {
@@ -263,7 +263,9 @@ int launch_gemm_presplit(int64_t m, int64_t n, int64_t k, const float* A, int64_
   if (!st) {
     const float scale = ldexpf(1.0f, scale_log2);
     const float inv_scale = ldexpf(1.0f, -scale_log2);
-    const tcec::FlagThresholds thr = tcec::flag_thresholds(V, R, scale_log2);
+    const float inv_scale2 = ldexpf(1.0f, -2 * scale_log2);
+    const tcec::FlagThresholds thr = S == tcec::kSchPlain ? tcec::plain_thresholds(V, R)
+                                                          : tcec::flag_thresholds(V, R, scale_log2);
     const unsigned ga = static_cast<unsigned>(((m + 63) / 64) * ((k + 63) / 64));
     tcec::tcec_presplit_kernel<V, R, false><<<ga, 256, 0, stream>>>(
         A, static_cast<int32_t>(m), static_cast<int32_t>(k), lda, ah, al, ldk,
@@ -283,7 +285,7 @@ int launch_gemm_presplit(int64_t m, int64_t n, int64_t k, const float* A, int64_
     shp.mma_order = 0;
     const int64_t pairs = ((m + 2 * Cfg::BM - 1) / (2 * Cfg::BM)) * ((n + Cfg::BN - 1) / Cfg::BN);
     kern<<<static_cast<unsigned>(2 * pairs), Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream>>>(
-        tmAh, tmAl, tmBh, tmBl, tmC, shp, inv_scale, d_flags);
+        tmAh, tmAl, tmBh, tmBl, tmC, shp, inv_scale, inv_scale2, d_flags);
     g_launches.fetch_add(3, std::memory_order_relaxed);
     if (cudaGetLastError() != cudaSuccess) st = TCEC_ERR_CUDA;
   }
@@ -294,11 +296,22 @@ int launch_gemm_presplit(int64_t m, int64_t n, int64_t k, const float* A, int64_
 template <int V, int R>
 int dispatch_bn(int bn, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda,
                 const float* B, int64_t ldb, float* C, int64_t ldc, int s, int de, int gm, int pf,
-                int kv, int mo, int sm, uint32_t* fl, cudaStream_t st) {
-  if (sm == 2) {
-    if (bn != 256 || kv != 0 || mo != 0) return TCEC_ERR_UNSUPPORTED;
-    return launch_gemm_presplit<V, R>(m, n, k, A, lda, B, ldb, C, ldc, s, de,
-                                      gm / 2 > 0 ? gm / 2 : 1, fl, st);
+                int kv, int mo, int sm, int sch, uint32_t* fl, cudaStream_t st) {
+  if (sm == 2 || sch != TCEC_SCHEME_CORRECTED3) {
+    if ((bn != 256 && bn != 0) || kv != 0 || mo != 0) return TCEC_ERR_UNSUPPORTED;
+    const int g = gm / 2 > 0 ? gm / 2 : 1;
+    switch (sch) {
+      case TCEC_SCHEME_CORRECTED3:
+        return launch_gemm_presplit<V, R, tcec::kSchC3>(m, n, k, A, lda, B, ldb, C, ldc, s, de, g, fl, st);
+      case TCEC_SCHEME_CORRECTED3_DD:
+        return launch_gemm_presplit<V, R, tcec::kSchC3DD>(m, n, k, A, lda, B, ldb, C, ldc, s, de, g, fl, st);
+      case TCEC_SCHEME_TC_PLAIN:
+        return launch_gemm_presplit<V, R, tcec::kSchPlain>(m, n, k, A, lda, B, ldb, C, ldc, 0, de, g, fl, st);
+      case TCEC_SCHEME_INUNIT4:
+        return launch_gemm_presplit<V, R, tcec::kSchIn4>(m, n, k, A, lda, B, ldb, C, ldc, s, de, g, fl, st);
+      default:
+        return TCEC_ERR_UNSUPPORTED;
+    }
   }
   switch (bn) {
     case 256:
@@ -386,7 +399,9 @@ int tcec_sgemm(int variant, int64_t m, int64_t n, int64_t k, const float* A, int
   if (opts) o = *opts;
   const int rounding = resolve_rounding(variant, o.split_rounding);
   if (!rounding_supported(variant, rounding)) return TCEC_ERR_UNSUPPORTED;
-  int scale_log2 = o.scale_log2 < 0 ? (variant == TCEC_FP16 ? 11 : 0) : o.scale_log2;
+  int scale_log2 = o.scale_log2 < 0 ? (variant == TCEC_FP16 && o.scheme != TCEC_SCHEME_INUNIT4 &&
+                                        o.scheme != TCEC_SCHEME_TC_PLAIN ? 11 : 0)
+                                     : o.scale_log2;
   if (variant == TCEC_TF32 && scale_log2 != 0) return TCEC_ERR_UNSUPPORTED;
   if (variant == TCEC_FP16 && scale_log2 != 0 && scale_log2 != 11) return TCEC_ERR_UNSUPPORTED;
   const int bk_op = variant == TCEC_FP16 ? 64 : 32;
@@ -410,6 +425,10 @@ int tcec_sgemm(int variant, int64_t m, int64_t n, int64_t k, const float* A, int
   // split_mode: 0 / 1 = split fused into the GEMM, 2 = split once in a separate pass
   const int split_mode = o.split_mode;
   if (split_mode < 0 || split_mode > 2) return TCEC_ERR_UNSUPPORTED;
+  // scheme: product schedule (TCEC_SCHEME_*); the comparators run in split-once mode
+  const int scheme = o.scheme;
+  if (scheme < TCEC_SCHEME_CORRECTED3 || scheme > TCEC_SCHEME_INUNIT4) return TCEC_ERR_UNSUPPORTED;
+  if (scheme == TCEC_SCHEME_INUNIT4 && o.scale_log2 > 0) return TCEC_ERR_UNSUPPORTED;
   if (m == 0 || n == 0) return TCEC_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (k == 0) {
@@ -426,21 +445,21 @@ int tcec_sgemm(int variant, int64_t m, int64_t n, int64_t k, const float* A, int
   if (variant == TCEC_FP16) {
     if (rounding == TCEC_ROUND_RN)
       return dispatch_bn<tcec::kFP16, tcec::kRN>(block_n, m, n, k, A, lda, B, ldb, C, ldc,
-                                                 scale_log2, drain_every, group_m, prefetch, kvariant, mma_order, split_mode, d_flags, st);
+                                                 scale_log2, drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, d_flags, st);
     if (rounding == TCEC_ROUND_RZ)
       return dispatch_bn<tcec::kFP16, tcec::kRZ>(block_n, m, n, k, A, lda, B, ldb, C, ldc,
-                                                 scale_log2, drain_every, group_m, prefetch, kvariant, mma_order, split_mode, d_flags, st);
+                                                 scale_log2, drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, d_flags, st);
     return TCEC_ERR_UNSUPPORTED;
   }
   if (rounding == TCEC_ROUND_RNA)
     return dispatch_bn<tcec::kTF32, tcec::kRNA>(block_n, m, n, k, A, lda, B, ldb, C, ldc, 0,
-                                                drain_every, group_m, prefetch, kvariant, mma_order, split_mode, d_flags, st);
+                                                drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, d_flags, st);
   if (rounding == TCEC_ROUND_RN)
     return dispatch_bn<tcec::kTF32, tcec::kRN>(block_n, m, n, k, A, lda, B, ldb, C, ldc, 0,
-                                               drain_every, group_m, prefetch, kvariant, mma_order, split_mode, d_flags, st);
+                                               drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, d_flags, st);
   if (rounding == TCEC_ROUND_RZ)
     return dispatch_bn<tcec::kTF32, tcec::kRZ>(block_n, m, n, k, A, lda, B, ldb, C, ldc, 0,
-                                               drain_every, group_m, prefetch, kvariant, mma_order, split_mode, d_flags, st);
+                                               drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, d_flags, st);
   return TCEC_ERR_UNSUPPORTED;
 }
 

@@ -139,23 +139,47 @@ __global__ void __launch_bounds__(256)
 }
 
 // ---------------------------------------------------------------------------
-// Three-product GEMM over pre-split operands.
-template <int V>
+// GEMM over pre-split operands.  The product schedule is a template parameter
+// so the same pipeline also runs the reference's in-unit comparator schemes on
+// the tensor core:
+//   kSchC3    corrected3: dC += dA*B_hi, A_hi*dB (one TMEM accumulator over all
+//             k), P = A_hi*B_hi drained into an FP32 RN register sum every
+//             drain interval, C = RN(C + dC 2^-s)      (schemes.py:265-307)
+//   kSchC3DD  corrected3 plus the dA*dB chain in its own accumulator, added
+//             last as RN(C + ddC 2^-2s)              (schemes.py:308-313)
+//   kSchPlain tc_plain: one product of the converted inputs, accumulated in
+//             the unit over all k                    (schemes.py:343-351)
+//   kSchIn4   markidis4 / corrected4 (hardware terminal): dA*dB, dA*B, A*dB,
+//             A*B per k-step into one accumulator    (schemes.py:352-364)
+enum Schedule : int { kSchC3 = 0, kSchC3DD = 1, kSchPlain = 2, kSchIn4 = 3 };
+
+template <int V, int S = kSchC3>
 struct PsCfg {
-  static constexpr int BM = 128;           // rows per CTA (pair M = 256)
-  static constexpr int BN = 256;           // pair N
-  static constexpr int BN_CTA = 128;       // B rows (= C columns) loaded per CTA
-  static constexpr int NOP = 3;
-  static constexpr int TILE_BYTES = 128 * 128;             // 128 rows x 128-byte k chunk
-  static constexpr int OP_BYTES = 4 * TILE_BYTES;          // A_hi | A_lo | B_hi | B_lo
+  static constexpr int BM = 128;                         // rows per CTA (pair M = 256)
+  static constexpr int BN = S == kSchC3DD ? 128 : 256;   // pair N (3 accumulators need N <= 170)
+  static constexpr int BN_CTA = BN / 2;                  // B rows (= C columns) loaded per CTA
+  static constexpr int A_TILE = 128 * 128;               // 128 rows x 128-byte k chunk
+  static constexpr int B_TILE = BN_CTA * 128;
+  static constexpr bool kLo = S != kSchPlain;            // lo operands used
+  static constexpr int OP_BYTES = (kLo ? 2 : 1) * (A_TILE + B_TILE);  // A_hi [A_lo] B_hi [B_lo]
+  static constexpr int OFF_AHI = 0;
+  static constexpr int OFF_ALO = A_TILE;
+  static constexpr int OFF_BHI = kLo ? 2 * A_TILE : A_TILE;
+  static constexpr int OFF_BLO = OFF_BHI + B_TILE;
+  static constexpr int NOP = (192 * 1024) / OP_BYTES;    // 3 / 4 / 6 stages
   static constexpr int OFF_OP = 0;
   static constexpr int OFF_BAR = NOP * OP_BYTES;
   static constexpr int NUM_BARS = 2 * NOP + 2;
   static constexpr int SMEM_BYTES = OFF_BAR + NUM_BARS * 8 + 16;
-  static constexpr int TMEM_COLS = 512;    // P [0,256) | dC [256,512)
-  static constexpr int NUM_THREADS = 384;  // warps 0-3 control, 4-11 drain
+  static constexpr bool kDrain = S == kSchC3 || S == kSchC3DD;
+  static constexpr int NUM_ACC = S == kSchC3 ? 2 : (S == kSchC3DD ? 3 : 1);
+  static constexpr int TMEM_COLS = NUM_ACC * BN > 256 ? 512 : 256;  // P | dC | ddC
+  static constexpr int NUM_THREADS = 384;                // warps 0-3 control, 4-11 drain
   static constexpr int DRAIN_WARP0 = 4, NUM_DRAIN_WARPS = 8;
-  static constexpr int EPI_WARP_BYTES = 32 * 128 * 4;
+  static constexpr int DRAIN_COLS = BN / 2;
+  static constexpr int EPI_WARP_BYTES = 32 * DRAIN_COLS * 4;
+  static_assert(NUM_ACC * BN <= 512, "TMEM budget");
+  static_assert(OP_BYTES % 1024 == 0, "stage alignment");
   static_assert(NUM_DRAIN_WARPS * EPI_WARP_BYTES <= OFF_BAR, "epilogue staging reuses the ring");
 };
 
@@ -169,15 +193,16 @@ __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap
       : "memory");
 }
 
-template <int V>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PsCfg<V>::NUM_THREADS, 1)
+template <int V, int S>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PsCfg<V, S>::NUM_THREADS, 1)
     tcec_gemm_ps_kernel(const __grid_constant__ CUtensorMap tmAh,  // A_hi [m][k] box 128B x 128
                         const __grid_constant__ CUtensorMap tmAl,  // A_lo
                         const __grid_constant__ CUtensorMap tmBh,  // B_hi^T [n][k] box 128B x 128
                         const __grid_constant__ CUtensorMap tmBl,  // B_lo^T
                         const __grid_constant__ CUtensorMap tmC,   // C [m][n], box 32 x 32, SW128
-                        const GemmShape shp, const float inv_scale, uint32_t* __restrict__ flags) {
-  using C = PsCfg<V>;
+                        const GemmShape shp, const float inv_scale, const float inv_scale2,
+                        uint32_t* __restrict__ flags) {
+  using C = PsCfg<V, S>;
   using VC = VarCfg<V>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
@@ -210,7 +235,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PsCfg<V>::NUM_THREAD
   const int n_cta = n_pair + rank * C::BN_CTA;
   const int nop = shp.num_op_stages;
   const int de = shp.drain_every;
-  const int nintervals = (nop + de - 1) / de;
+  const int nintervals = C::kDrain ? (nop + de - 1) / de : 0;
 
   if (warp == 0 && lane == 0) {
     if (smem_base & 1023u) __trap();
@@ -234,6 +259,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PsCfg<V>::NUM_THREAD
   const uint32_t tmem_base = *tmem_slot;
   const uint32_t tmem_P = tmem_base;
   const uint32_t tmem_dC = tmem_base + C::BN;
+  const uint32_t tmem_ddC = tmem_base + 2 * C::BN;
 
   if (warp < C::DRAIN_WARP0) {
     if (warp == 0 && lane == 0) {
@@ -246,10 +272,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PsCfg<V>::NUM_THREAD
         const uint32_t dst = smem_base + C::OFF_OP + o * C::OP_BYTES;
         const uint32_t bar = leader_full + o * 8;
         const int kc = kb * VC::BK_OP;
-        tma_load_2d_pair(dst, &tmAh, bar, kc, m_cta);
-        tma_load_2d_pair(dst + C::TILE_BYTES, &tmAl, bar, kc, m_cta);
-        tma_load_2d_pair(dst + 2 * C::TILE_BYTES, &tmBh, bar, kc, n_cta);
-        tma_load_2d_pair(dst + 3 * C::TILE_BYTES, &tmBl, bar, kc, n_cta);
+        tma_load_2d_pair(dst + C::OFF_AHI, &tmAh, bar, kc, m_cta);
+        tma_load_2d_pair(dst + C::OFF_BHI, &tmBh, bar, kc, n_cta);
+        if constexpr (C::kLo) {
+          tma_load_2d_pair(dst + C::OFF_ALO, &tmAl, bar, kc, m_cta);
+          tma_load_2d_pair(dst + C::OFF_BLO, &tmBl, bar, kc, n_cta);
+        }
       }
     } else if (warp == 1 && lane == 0 && rank == 0) {
       // ===================== MMA issuer (leader CTA) =====================
@@ -261,28 +289,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PsCfg<V>::NUM_THREAD
         sm100::tc_fence_after();
         const uint32_t op = sm100::opaque(smem_base + C::OFF_OP + o * C::OP_BYTES) >> 4;
         const uint32_t ahi = op | (1u << 16);
-        const uint32_t alo = ahi + (C::TILE_BYTES >> 4);
-        const uint32_t bhi = ahi + (2 * C::TILE_BYTES >> 4);
-        const uint32_t blo = ahi + (3 * C::TILE_BYTES >> 4);
-        // corrections first (reference order per k-step: dA*B then A*dB), so the
-        // drain of the previous P overlaps them (schemes.py:294-298)
+        const uint32_t alo = ahi + (C::OFF_ALO >> 4);
+        const uint32_t bhi = ahi + (C::OFF_BHI >> 4);
+        const uint32_t blo = ahi + (C::OFF_BLO >> 4);
+        if constexpr (S == kSchPlain) {
 #pragma unroll
-        for (int ks = 0; ks < 4; ++ks) {
-          sm100::mma_pair_split<V == kTF32>(tmem_dC, alo + 2 * ks, hi_w, bhi + 2 * ks, hi_w, idesc,
-                                            (kb | ks) != 0);
-          sm100::mma_pair_split<V == kTF32>(tmem_dC, ahi + 2 * ks, hi_w, blo + 2 * ks, hi_w, idesc, 1u);
-        }
-        const bool first_in_interval = (kb % de) == 0;
-        if (first_in_interval && kb > 0) {
-          sm100::mbar_wait_cluster(p_empty, ((kb / de) - 1) & 1);
-          sm100::tc_fence_after();
-        }
+          for (int ks = 0; ks < 4; ++ks)
+            sm100::mma_pair_split<V == kTF32>(tmem_P, ahi + 2 * ks, hi_w, bhi + 2 * ks, hi_w, idesc,
+                                              (kb | ks) != 0);
+        } else if constexpr (S == kSchIn4) {
+          // the reference's four-call order per block: dA*dB, dA*B, A*dB, A*B
 #pragma unroll
-        for (int ks = 0; ks < 4; ++ks)
-          sm100::mma_pair_split<V == kTF32>(tmem_P, ahi + 2 * ks, hi_w, bhi + 2 * ks, hi_w, idesc,
-                                            !(first_in_interval && ks == 0));
+          for (int ks = 0; ks < 4; ++ks) {
+            sm100::mma_pair_split<V == kTF32>(tmem_P, alo + 2 * ks, hi_w, blo + 2 * ks, hi_w, idesc,
+                                              (kb | ks) != 0);
+            sm100::mma_pair_split<V == kTF32>(tmem_P, alo + 2 * ks, hi_w, bhi + 2 * ks, hi_w, idesc, 1u);
+            sm100::mma_pair_split<V == kTF32>(tmem_P, ahi + 2 * ks, hi_w, blo + 2 * ks, hi_w, idesc, 1u);
+            sm100::mma_pair_split<V == kTF32>(tmem_P, ahi + 2 * ks, hi_w, bhi + 2 * ks, hi_w, idesc, 1u);
+          }
+        } else {
+          // corrections first (reference order per k-step: dA*B then A*dB), so the
+          // drain of the previous P overlaps them (schemes.py:294-298)
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks) {
+            sm100::mma_pair_split<V == kTF32>(tmem_dC, alo + 2 * ks, hi_w, bhi + 2 * ks, hi_w, idesc,
+                                              (kb | ks) != 0);
+            sm100::mma_pair_split<V == kTF32>(tmem_dC, ahi + 2 * ks, hi_w, blo + 2 * ks, hi_w, idesc, 1u);
+            if constexpr (S == kSchC3DD)  // schemes.py:308-313: the dA*dB chain
+              sm100::mma_pair_split<V == kTF32>(tmem_ddC, alo + 2 * ks, hi_w, blo + 2 * ks, hi_w, idesc,
+                                                (kb | ks) != 0);
+          }
+          const bool first_in_interval = (kb % de) == 0;
+          if (first_in_interval && kb > 0) {
+            sm100::mbar_wait_cluster(p_empty, ((kb / de) - 1) & 1);
+            sm100::tc_fence_after();
+          }
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks)
+            sm100::mma_pair_split<V == kTF32>(tmem_P, ahi + 2 * ks, hi_w, bhi + 2 * ks, hi_w, idesc,
+                                              !(first_in_interval && ks == 0));
+        }
         sm100::mma_commit_pair_mc(&op_empty[o], 0x3);
-        if ((kb % de) == de - 1 || kb == nop - 1) sm100::mma_commit_pair_mc(p_full, 0x3);
+        if (kb == nop - 1 || (C::kDrain && (kb % de) == de - 1))
+          sm100::mma_commit_pair_mc(p_full, 0x3);
       }
     }
   } else {
@@ -291,16 +340,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PsCfg<V>::NUM_THREAD
     const int h = (warp - C::DRAIN_WARP0) >> 2;
     const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
     const uint32_t p_empty_leader = sm100::mapa_shared(sm100::smem_u32(p_empty), 0);
-    float acc[128];
+    constexpr int NC = C::DRAIN_COLS;
+    float acc[NC];
 #pragma unroll
-    for (int j = 0; j < 128; ++j) acc[j] = 0.0f;
+    for (int j = 0; j < NC; ++j) acc[j] = 0.0f;
     for (int it = 0; it < nintervals; ++it) {
       sm100::mbar_wait(p_full, it & 1);
       sm100::tc_fence_after();
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
+      for (int c = 0; c < NC / 16; ++c) {
         uint32_t r[16];
-        sm100::tmem_ld_32x32b_x16(tmem_P + lane_off + h * 128 + c * 16, r);
+        sm100::tmem_ld_32x32b_x16(tmem_P + lane_off + h * NC + c * 16, r);
         sm100::tmem_ld_wait();
 #pragma unroll
         for (int j = 0; j < 16; ++j)  // schemes.py:300-304: c = RN32(c + partial)
@@ -310,21 +360,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PsCfg<V>::NUM_THREAD
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive_remote(p_empty_leader);
     }
+    if constexpr (!C::kDrain) {
+      // in-unit schemes: the single accumulator is the result
+      sm100::mbar_wait(p_full, 0);
+      sm100::tc_fence_after();
+    }
     bool nonfinite = false;
     const uint32_t stage = smem_base + (warp - C::DRAIN_WARP0) * C::EPI_WARP_BYTES;
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
+    for (int b = 0; b < NC / 32; ++b) {
       const uint32_t box = stage + b * 4096;
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
+        const uint32_t col = lane_off + h * NC + b * 32 + c * 16;
         uint32_t r[16];
-        sm100::tmem_ld_32x32b_x16(tmem_dC + lane_off + h * 128 + b * 32 + c * 16, r);
+        sm100::tmem_ld_32x32b_x16((C::kDrain ? tmem_dC : tmem_P) + col, r);
         sm100::tmem_ld_wait();
+        uint32_t rr[16];
+        if constexpr (S == kSchC3DD) {
+          sm100::tmem_ld_32x32b_x16(tmem_ddC + col, rr);
+          sm100::tmem_ld_wait();
+        }
         float o[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          // schemes.py:306-307: one rounding of c + dC * 2^-s
-          o[j] = __fmaf_rn(__uint_as_float(r[j]), inv_scale, acc[b * 32 + c * 16 + j]);
+          if constexpr (C::kDrain) {
+            // schemes.py:306-307: one rounding of c + dC * 2^-s
+            o[j] = __fmaf_rn(__uint_as_float(r[j]), inv_scale, acc[b * 32 + c * 16 + j]);
+            if constexpr (S == kSchC3DD)  // schemes.py:312-313: then + ddC * 2^-2s
+              o[j] = __fmaf_rn(__uint_as_float(rr[j]), inv_scale2, o[j]);
+          } else {
+            o[j] = __uint_as_float(r[j]);
+          }
           nonfinite |= !isfinite(o[j]);
         }
 #pragma unroll
@@ -334,7 +401,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PsCfg<V>::NUM_THREAD
       sm100::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-        sm100::tma_store_2d(&tmC, smem + (box - smem_base), n_pair + h * 128 + b * 32, m_cta + q * 32);
+        sm100::tma_store_2d(&tmC, smem + (box - smem_base), n_pair + h * NC + b * 32, m_cta + q * 32);
         sm100::tma_store_commit();
       }
     }

@@ -167,22 +167,56 @@ def drain_k_for(variant: int, block_k: int) -> int:
     return max(DEFAULT_DRAIN_K[variant], stage * max(1, -(-int(block_k) // stage)))
 
 
-def resolve_scheme(scheme) -> tuple[int, int, int]:
-    """(variant, rounding code, scale_log2) for a corrected3 scheme.
+# Product schedules of the kernel (include/tcec.h TCEC_SCHEME_*).
+SCHED_CORRECTED3, SCHED_CORRECTED3_DD, SCHED_TC_PLAIN, SCHED_INUNIT4 = 0, 1, 2, 3
 
-    Accepts a registry name, this package's GemmScheme, or the reference's
-    GemmScheme (duck-typed on .kind.value and .split).
-    """
+
+def resolve_scheme(scheme) -> tuple[int, int, int]:
+    """(variant, rounding code, scale_log2) for a corrected3 scheme (the
+    accelerated path).  Accepts a registry name, this package's GemmScheme, or
+    the reference's GemmScheme (duck-typed on .kind.value and .split)."""
+    variant, rounding, scale, sched = resolve_schedule(scheme)
+    if sched != SCHED_CORRECTED3:
+        raise NotImplementedError(f"{getattr(scheme, 'label', scheme)!r} is not a corrected3 scheme")
+    return variant, rounding, scale
+
+
+def resolve_schedule(scheme) -> tuple[int, int, int, int]:
+    """(variant, rounding code, scale_log2, product schedule) of any scheme the
+    tensor core can run: corrected3 (the accelerated path) and the reference's
+    in-unit comparators tc_plain (schemes.py:343-351) and markidis4 /
+    corrected4 with the RZ terminal (schemes.py:352-364) -- the hardware
+    accumulator's terminal rounding is fixed, so corrected4 with an RN
+    terminal is emulator-only.  fp64_ref / fp32_simt / fp32_lsbtrunc are the
+    reference's CPU baselines and are not run here."""
     if isinstance(scheme, str):
         if scheme not in SCHEMES_BY_NAME:
             raise ValueError(f"unknown scheme name: {scheme!r}")
         scheme = SCHEMES_BY_NAME[scheme]
     kind = getattr(getattr(scheme, "kind", None), "value", None)
-    if kind != GemmKind.CORRECTED3.value:
-        raise NotImplementedError(
-            f"scheme kind {kind!r} is a CPU comparator of the reference; only corrected3 "
-            "(FP16-TCEC / TF32-TCEC) runs on the sm_100a path")
-    return native_split_args(scheme.split)
+    if kind == GemmKind.CORRECTED3.value:
+        return (*native_split_args(scheme.split), SCHED_CORRECTED3)
+    if kind == GemmKind.TC_PLAIN.value:
+        f = getattr(scheme, "conv_format", None)
+        fmt = (getattr(f, "exp_bits", None), getattr(f, "man_bits", None))
+        if fmt == (5, 10):  # FP16, converted RN (schemes.py:346)
+            return N.TCEC_FP16, N.ROUND_RN, 0, SCHED_TC_PLAIN
+        if fmt == (8, 10):  # TF32, converted RNA
+            return N.TCEC_TF32, N.ROUND_RNA, 0, SCHED_TC_PLAIN
+        raise NotImplementedError(f"tc_plain in {f!r} has no tensor-core kind here")
+    if kind in (GemmKind.MARKIDIS4.value, GemmKind.CORRECTED4.value):
+        term = getattr(getattr(scheme, "terminal", None), "value", "rz")
+        if kind == GemmKind.CORRECTED4.value and term != "rz":
+            raise NotImplementedError(
+                "corrected4 with an RN terminal is emulator-only: the tensor core's "
+                "accumulator rounding is fixed (run corrected4_rz / markidis4 on hardware)")
+        variant, rounding, scale = native_split_args(scheme.split)
+        if scale != 0:
+            raise ValueError("in-unit four-term schemes require an unscaled split")
+        return variant, rounding, 0, SCHED_INUNIT4
+    raise NotImplementedError(
+        f"scheme kind {kind!r} is a CPU baseline of the reference; the sm_100a path runs "
+        "corrected3 (FP16-TCEC / TF32-TCEC) and the in-unit tensor-core comparators")
 
 
 def _is_torch(x) -> bool:
@@ -244,7 +278,7 @@ def gemm_device(a, b, scheme="corrected3_halfhalf", cfg: MmaConfig | None = None
     """
     import torch
 
-    variant, rounding, scale = resolve_scheme(scheme)
+    variant, rounding, scale, sched = resolve_schedule(scheme)
     if a.dim() != 2 or b.dim() != 2:
         raise ValueError("gemm expects 2-D matrices")
     m, k = a.shape
@@ -267,7 +301,7 @@ def gemm_device(a, b, scheme="corrected3_halfhalf", cfg: MmaConfig | None = None
     opts = N.make_opts(split_rounding=rounding, scale_log2=scale,
                        drain_k=dk, block_n=block_n, group_m=group_m,
                        prefetch=prefetch, kernel_variant=kernel_variant,
-                       mma_order=mma_order, split_mode=split_mode)
+                       mma_order=mma_order, split_mode=split_mode, scheme=sched)
     A, lda = _tma_ready(a)
     B, ldb = _tma_ready(b)
     C, ldc = out, out.stride(0)
@@ -292,7 +326,7 @@ def gemm(a, b, scheme, cfg: MmaConfig | None = None, out=None) -> GemmRun:
     float32 ndarray (e.g. in pinned memory) for host inputs, a CUDA tensor for
     device inputs.
     """
-    variant, rounding, scale = resolve_scheme(scheme)
+    variant, rounding, scale, sched = resolve_schedule(scheme)
     block_k = cfg.block_k if cfg is not None else 16
     if _is_torch(a) and a.is_cuda:
         import torch
@@ -326,8 +360,52 @@ def gemm(a, b, scheme, cfg: MmaConfig | None = None, out=None) -> GemmRun:
         C = np.empty((m, n), dtype=np.float32)
     fl = ctypes.c_uint32(0)
     opts = N.make_opts(split_rounding=rounding, scale_log2=scale,
-                       drain_k=drain_k_for(variant, block_k))
+                       drain_k=drain_k_for(variant, block_k), scheme=sched)
     N.check(N.lib().tcec_sgemm_host(variant, m, n, k, A.ctypes.data, max(k, 1), B.ctypes.data,
                                     max(n, 1), C.ctypes.data, max(n, 1), ctypes.byref(opts),
                                     ctypes.byref(fl), None), "tcec_sgemm_host")
     return GemmRun(m=m, n=n, k=k, scheme=scheme, output=C, flags=_flags_to_run(int(fl.value)))
+
+
+def _ulp_fp32(x: np.ndarray) -> np.ndarray:
+    """schemes.py:412-415."""
+    _, e2 = np.frexp(np.abs(x))
+    e = np.clip(e2 - 1, -126, 127)
+    return np.ldexp(1.0, e - 23)
+
+
+def delta_term_ablation(a, b, split: SplitScheme | None = None, cfg: MmaConfig | None = None,
+                        ) -> tuple[GemmRun, GemmRun, float]:
+    """schemes.py:418-451 on the tensor core: the three-term scheme and its
+    four-term sibling (the dA*dB chain in a separate accumulator, added last
+    with scale 2^-2s) on the same splits.  Returns both runs and the largest
+    elementwise difference in FP32 ulps of the four-term output."""
+    if split is None:
+        split = scaled_halfhalf()
+    scheme3 = corrected3(split)
+    variant, rounding, scale = native_split_args(split)
+    A = _as_fp32_host(a.cpu().numpy() if _is_torch(a) else a)
+    B = _as_fp32_host(b.cpu().numpy() if _is_torch(b) else b)
+    m, k = A.shape
+    kb, n = B.shape
+    if kb != k:
+        raise ValueError(f"inner dimensions differ: {k} vs {kb}")
+    block_k = cfg.block_k if cfg is not None else 16
+    outs = []
+    for sched in (SCHED_CORRECTED3, SCHED_CORRECTED3_DD):
+        C = np.empty((m, n), dtype=np.float32)
+        fl = ctypes.c_uint32(0)
+        opts = N.make_opts(split_rounding=rounding, scale_log2=scale,
+                           drain_k=drain_k_for(variant, block_k), scheme=sched)
+        N.check(N.lib().tcec_sgemm_host(variant, m, n, k, np.ascontiguousarray(A).ctypes.data,
+                                        max(k, 1), np.ascontiguousarray(B).ctypes.data, max(n, 1),
+                                        C.ctypes.data, max(n, 1), ctypes.byref(opts),
+                                        ctypes.byref(fl), None), "tcec_sgemm_host")
+        outs.append((C, _flags_to_run(int(fl.value))))
+    (c3, f3), (c4, _) = outs
+    run3 = GemmRun(m, n, k, scheme3, c3, f3)
+    run4 = GemmRun(m, n, k, GemmScheme(GemmKind.CORRECTED4, split=split, terminal=RoundingMode.RZ),
+                   c4, f3)
+    diff = np.abs(c3.astype(np.float64) - c4.astype(np.float64))
+    max_ulp = float(np.max(diff / _ulp_fp32(c4.astype(np.float64)))) if diff.size else 0.0
+    return run3, run4, max_ulp

@@ -172,8 +172,50 @@ def generator_goldens():
     np.savez_compressed(os.path.join(OUT, "genmat_golden.npz"), **out)
 
 
+def inunit_goldens():
+    """The reference's in-unit comparator schemes (schemes.py:343-364), which
+    the GPU also runs on the tensor core: pins oracle.inunit bit for bit."""
+    G = tcgemm.generate
+    MS = tcgemm.MatrixSpec
+    cases = []
+    for seed in (0, 1):
+        a = G(MS(8, 64, tcgemm.Urand(-1, 1), seed))
+        b = G(MS(64, 8, tcgemm.Urand(-1, 1), tcgemm.pair_seed(seed)))
+        cases.append((f"urand_s{seed}_8x8x64", a, b))
+    a = G(MS(6, 1024, tcgemm.Urand(-1, 1), 5))
+    b = G(MS(1024, 6, tcgemm.Urand(-1, 1), tcgemm.pair_seed(5)))
+    cases.append(("urand_6x6x1024", a, b))
+    a = G(MS(8, 128, tcgemm.ExpRand(-15, 15), 11))
+    b = G(MS(128, 8, tcgemm.ExpRand(-15, 15), 12))
+    cases.append(("exprand_8x8x128", a, b))
+    a, b = tcgemm.type_pair(2, 8, 8, 96, 3)
+    cases.append(("type2_8x8x96", a, b))
+    a = G(MS(4, 40, tcgemm.ExpRand(-40, -20), 13))  # FP16 conversion vanishes
+    b = G(MS(40, 4, tcgemm.Urand(-1, 1), 14))
+    cases.append(("tiny_4x4x40", a, b))
+    a = G(MS(4, 48, tcgemm.ExpRand(14, 16), 21))    # FP16 conversion overflows
+    b = G(MS(48, 4, tcgemm.Urand(-1, 1), 22))
+    cases.append(("overflow_4x4x48", a, b))
+    schemes = {name: tcgemm.SCHEMES_BY_NAME[name] for name in
+               ("tc_plain_fp16", "tc_plain_tf32", "markidis4", "corrected4_rn", "corrected4_rz")}
+    schemes["markidis4_tf32"] = tcgemm.markidis4(TF32)
+    out = {"names": np.array([c[0] for c in cases]), "schemes": np.array(list(schemes))}
+    for tag, a, b in cases:
+        out[f"{tag}__A"], out[f"{tag}__B"] = a, b
+        for sname, sch in schemes.items():
+            run = tcgemm.gemm(a, b, sch)
+            out[f"{tag}__{sname}__C"] = run.output
+            out[f"{tag}__{sname}__flags"] = np.array(
+                [run.flags.saw_overflow, run.flags.saw_out_of_range], dtype=np.int8)
+    np.savez_compressed(os.path.join(OUT, "inunit_golden.npz"), **out)
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["inunit"]:
+        inunit_goldens()
+        sys.exit(0)
     split_goldens()
     generator_goldens()
     gemm_goldens()
+    inunit_goldens()
     print("wrote", sorted(f for f in os.listdir(OUT) if f.endswith(".npz")))

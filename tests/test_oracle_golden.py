@@ -136,3 +136,16 @@ def test_generators_match_reference():
     for t in (1, 2, 3, 4):
         a, b = O.type_pair(t, 3, 4, 5, 9)
         assert np.array_equal(a, g[f"type{t}_A"]) and np.array_equal(b, g[f"type{t}_B"])
+
+
+def test_inunit_comparators_match_reference_goldens():
+    """oracle.inunit (tc_plain, markidis4, corrected4 RN/RZ; schemes.py:343-364)
+    equals the reference's gemm bit for bit, flags included."""
+    g = np.load(os.path.join(GOLD, "inunit_golden.npz"))
+    for tag in g["names"]:
+        a, b = g[f"{tag}__A"], g[f"{tag}__B"]
+        for sname in g["schemes"]:
+            c, fl = O.inunit(a, b, str(sname))
+            _same(c, g[f"{tag}__{sname}__C"])
+            ov, oor = g[f"{tag}__{sname}__flags"]
+            assert (bool(fl & 1), bool(fl & 2)) == (bool(ov), bool(oor)), (tag, sname, fl)
