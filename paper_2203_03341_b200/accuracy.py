@@ -7,9 +7,15 @@ bit-exactly in genmat.py here) and the same metric (Eq. 7, analysis.py:175-192).
 The hot path runs on the GPU; the FP64 ground truth is cuBLAS DGEMM on the GPU
 (the reference's sequential FP64 sum differs from it at the 1e-16 level).
 
-Schemes: corrected3_halfhalf / corrected3_tf32 (this package's kernels) and
-`cublas_sgemm` (FP32 SIMT SGEMM, TF32 disabled) as the SGEMM baseline; the
-reference's other CPU comparators are out of scope.
+Schemes: corrected3_halfhalf / corrected3_tf32 (the accelerated path), the
+reference's in-unit comparators run on the tensor core (tc_plain_fp16,
+tc_plain_tf32, markidis4, corrected4_rz -- the hardware's own accumulator
+rounding), and `cublas_sgemm` (FP32 SIMT SGEMM, TF32 disabled) as the SGEMM
+baseline.  `ablate-delta` mirrors cli.py:196-214 (three- vs four-term
+correction, delta_term_ablation) and `rounding-ablation` is the hardware
+analogue of cli.py:173-193: the tensor core's terminal rounding cannot be
+switched, so it reports the in-unit four-term scheme (corrected4_rz on the
+hardware) against corrected3 (accumulation moved out of the unit) and SGEMM.
 
     python -m paper_2203_03341_b200.accuracy gemm-accuracy --m 16 --n 16 \
         --k 256,1024,4096 --scheme corrected3_halfhalf,cublas_sgemm --dist urand:-1,1
@@ -25,7 +31,8 @@ import numpy as np
 
 from .genmat import ExpRand, MatrixSpec, Urand, generate, pair_seed, type_pair
 
-GPU_SCHEMES = ("corrected3_halfhalf", "corrected3_tf32", "cublas_sgemm")
+GPU_SCHEMES = ("corrected3_halfhalf", "corrected3_tf32", "tc_plain_fp16", "tc_plain_tf32",
+               "markidis4", "corrected4_rz", "cublas_sgemm")
 
 
 def _fmt64(x: float) -> str:
@@ -128,19 +135,91 @@ def gemm_accuracy(ms, ns, ks, schemes, dist, seeds, block_k: int = 16) -> list[s
     return lines
 
 
+def _residual(ref, out) -> float:
+    """analysis.py:175-192 (Eq. 7) against the FP64 product on the GPU."""
+    import torch
+
+    den = float(torch.linalg.norm(ref))
+    num = float(torch.linalg.norm(ref - torch.as_tensor(out, device=ref.device).double()))
+    return 0.0 if den == 0.0 and num == 0.0 else num / den
+
+
+def _sizes_seeds(ms, ns, ks, seeds, dist, what):
+    if isinstance(dist, tuple):
+        raise ValueError(f"{what} takes urand or exprand distributions")
+    for m in ms:
+        for n in ns:
+            for k in ks:
+                for seed in seeds:
+                    yield m, n, k, seed
+
+
+def ablate_delta(ms, ns, ks, dist, seeds, block_k: int = 16) -> list[str]:
+    """cmd_ablate_delta (cli.py:196-214) on the tensor core."""
+    import torch
+
+    from .schemes import MmaConfig, delta_term_ablation
+
+    lines = ["m,n,k,seed,residual_3term,residual_4term,max_ulp_diff"]
+    for m, n, k, seed in _sizes_seeds(ms, ns, ks, seeds, dist, "ablate-delta"):
+        a, b = input_pair(dist, m, n, k, seed)
+        ref = torch.from_numpy(a).cuda().double() @ torch.from_numpy(b).cuda().double()
+        run3, run4, max_ulp = delta_term_ablation(a, b, cfg=MmaConfig(block_k=block_k))
+        lines.append(f"{m},{n},{k},{seed},{_fmt64(_residual(ref, run3.output))},"
+                     f"{_fmt64(_residual(ref, run4.output))},{_fmt64(max_ulp)}")
+    return lines
+
+
+def rounding_ablation(ms, ns, ks, dist, seeds, block_k: int = 16) -> list[str]:
+    """Hardware analogue of cmd_rounding_ablation (cli.py:173-193): the in-unit
+    four-term scheme with the tensor core's own terminal rounding against
+    corrected3 (main-term accumulation moved out of the unit, RN adds) and
+    cuBLAS SGEMM."""
+    import torch
+
+    from .schemes import MmaConfig, gemm
+
+    cfg = MmaConfig(block_k=block_k)
+    prev_tf32 = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    lines = ["m,n,k,seed,residual_inunit_hw,residual_corrected3,residual_fp32"]
+    try:
+        for m, n, k, seed in _sizes_seeds(ms, ns, ks, seeds, dist, "rounding-ablation"):
+            a, b = input_pair(dist, m, n, k, seed)
+            A, B = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+            ref = A.double() @ B.double()
+            r4 = _residual(ref, gemm(A, B, "corrected4_rz", cfg).output)
+            r3 = _residual(ref, gemm(A, B, "corrected3_halfhalf", cfg).output)
+            r32 = _residual(ref, A @ B)
+            lines.append(f"{m},{n},{k},{seed},{_fmt64(r4)},{_fmt64(r3)},{_fmt64(r32)}")
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev_tf32
+    return lines
+
+
+def _add_size_flags(p, default_k: str) -> None:
+    p.add_argument("--m", default="16")
+    p.add_argument("--n", default="16")
+    p.add_argument("--k", default=default_k)
+    p.add_argument("--seeds", default="0,1,2,3,4,5,6,7")
+    p.add_argument("--block-k", type=int, default=16, help="drain interval request (MmaConfig.block_k)")
+
+
 def _build_parser() -> argparse.ArgumentParser:
     parser = argparse.ArgumentParser(prog="tcec-accuracy",
                                      description="GPU error-corrected GEMM accuracy (CSV).")
     parser.add_argument("--out", default=None, help="output path (default: stdout)")
     sub = parser.add_subparsers(dest="command", required=True)
     p = sub.add_parser("gemm-accuracy", help="relative residuals per scheme")
-    p.add_argument("--m", default="16")
-    p.add_argument("--n", default="16")
-    p.add_argument("--k", default="256,1024,4096")
-    p.add_argument("--seeds", default="0,1,2,3,4,5,6,7")
-    p.add_argument("--block-k", type=int, default=16, help="drain interval request (MmaConfig.block_k)")
+    _add_size_flags(p, "256,1024,4096")
     p.add_argument("--scheme", default="corrected3_halfhalf,cublas_sgemm")
     p.add_argument("--dist", default="urand:-1,1", help="urand:lo,hi | exprand:a,b | type:1..4")
+    p = sub.add_parser("rounding-ablation", help="in-unit (hardware rounding) vs corrected3 vs SGEMM")
+    _add_size_flags(p, "16,256,1024,4096")
+    p.add_argument("--dist", default="urand:-1,1")
+    p = sub.add_parser("ablate-delta", help="three-term vs four-term correction")
+    _add_size_flags(p, "16,1024")
+    p.add_argument("--dist", default="urand:-1,1")
     return parser
 
 
@@ -148,10 +227,16 @@ def main(argv: list[str] | None = None) -> int:
     """cli.py:268-281: CSV to stdout or --out; ValueError -> 'error: ...', exit 1."""
     args = _build_parser().parse_args(argv)
     try:
-        lines = gemm_accuracy(_parse_int_list(args.m), _parse_int_list(args.n),
-                              _parse_int_list(args.k),
-                              [s.strip() for s in args.scheme.split(",") if s.strip()],
-                              parse_dist(args.dist), _parse_int_list(args.seeds), args.block_k)
+        sizes = (_parse_int_list(args.m), _parse_int_list(args.n), _parse_int_list(args.k))
+        if args.command == "gemm-accuracy":
+            lines = gemm_accuracy(*sizes, [s.strip() for s in args.scheme.split(",") if s.strip()],
+                                  parse_dist(args.dist), _parse_int_list(args.seeds), args.block_k)
+        elif args.command == "ablate-delta":
+            lines = ablate_delta(*sizes, parse_dist(args.dist), _parse_int_list(args.seeds),
+                                 args.block_k)
+        else:
+            lines = rounding_ablation(*sizes, parse_dist(args.dist), _parse_int_list(args.seeds),
+                                      args.block_k)
     except ValueError as exc:
         print(f"error: {exc}", file=sys.stderr)
         return 1

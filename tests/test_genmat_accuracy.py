@@ -71,3 +71,33 @@ def test_gemm_accuracy_csv_on_gpu(tmp_path):
                    "--scheme", "corrected3_halfhalf", "--dist", "type:4"])
     assert rc == 0
     assert "out_of_range" in out.read_text()
+
+
+def test_ablation_cli_rejects_type_distributions(capsys):
+    assert ACC.main(["ablate-delta", "--dist", "type:2"]) == 1
+    assert ACC.main(["rounding-ablation", "--dist", "type:2"]) == 1
+    assert "error:" in capsys.readouterr().err
+
+
+@pytest.mark.gpu
+def test_ablation_csvs_on_gpu(tmp_path):
+    """The paper's two ablations on the tensor core (cli.py:173-214 analogues)."""
+    out = tmp_path / "abl.csv"
+    assert ACC.main(["--out", str(out), "ablate-delta", "--k", "16,1024", "--seeds", "0,1"]) == 0
+    lines = out.read_text().strip().splitlines()
+    assert lines[0] == "m,n,k,seed,residual_3term,residual_4term,max_ulp_diff"
+    for ln in lines[1:]:
+        r3, r4 = (float(x) for x in ln.split(",")[4:6])
+        assert r3 < 1e-6 and r4 < 1e-6 and abs(r3 - r4) <= 0.1 * r4
+    assert ACC.main(["--out", str(out), "rounding-ablation", "--k", "4096", "--seeds", "0,1"]) == 0
+    lines = out.read_text().strip().splitlines()
+    assert lines[0] == "m,n,k,seed,residual_inunit_hw,residual_corrected3,residual_fp32"
+    for ln in lines[1:]:
+        r_in, r3, _ = (float(x) for x in ln.split(",")[4:7])
+        assert r_in > 2 * r3
+    rc = ACC.main(["--out", str(out), "gemm-accuracy", "--k", "1024", "--seeds", "0,1",
+                   "--scheme", "tc_plain_fp16,tc_plain_tf32,markidis4,corrected4_rz"])
+    assert rc == 0
+    avg = {ln.split(",")[3]: float(ln.split(",")[5])
+           for ln in out.read_text().splitlines() if ",avg," in ln}
+    assert avg["tc_plain_fp16"] > 1e-4 and avg["markidis4"] < 1e-4
