@@ -74,7 +74,7 @@ def load_peaks():
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    Q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -91,7 +91,11 @@ class ClockSampler:
         except Exception:
             self.proc = None
 
-    def stop(self):
+    def stop(self, window=None):
+        """Median SM clock over the samples taken inside `window` = (t0, t1)
+        (epoch seconds of the timed region; all samples when None)."""
+        from datetime import datetime
+
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -106,6 +110,13 @@ class ClockSampler:
             parts = [x.strip() for x in line.split(",")]
             if len(parts) < 9:
                 continue
+            if window is not None:
+                try:
+                    ts = datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                except ValueError:
+                    ts = None
+                if ts is not None and not (window[0] <= ts <= window[1]):
+                    continue
             try:
                 sm.append(float(parts[1]))
                 mx.append(float(parts[2]))
@@ -122,32 +133,33 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ CPU oracle ---
-def cpu_oracle_sample(variant: str, k: int, seconds: float, threads: int):
+def cpu_oracle_sample(variant: str, k: int, seconds: float, threads: int, rows: int | None = None):
     """Time the CPU oracle (test-infrastructure restatement of the reference's
     corrected3 path, oracle/tcec_oracle.c) on a sub-block rows x cols x k of
     the workload, sized to take about `seconds` on `threads` host threads."""
     from oracle import oracle as O
 
     bk = 16 if variant == "fp16" else 8
-    # calibrate on threads x 8 outputs, then size a threads*R x 64 block
-    a = O.urand(threads, k, -1, 1, 11)
-    b = O.urand(k, 8, -1, 1, O.pair_seed(11))
-    t0 = time.perf_counter()
-    O.corrected3(a, b, variant, block_k=bk, nthreads=threads)
-    t_small = max(time.perf_counter() - t0, 1e-4)
     cols = 64
-    reps = max(1, int(round(seconds / (t_small * cols / 8))))
-    rows = min(threads * reps, 8192)
-    a = O.urand(rows, k, -1, 1, 12)
-    b = O.urand(k, cols, -1, 1, O.pair_seed(12))
-    t0 = time.perf_counter()
-    O.corrected3(a, b, variant, block_k=bk, nthreads=threads)
-    dt = time.perf_counter() - t0
+    # grow the output block until one run takes about `seconds` (per-call fixed
+    # costs -- splitting B, thread start-up -- dominate tiny calibration runs)
+    fixed = rows is not None
+    rows = rows or threads
+    while True:
+        a = O.urand(rows, k, -1, 1, 12)
+        b = O.urand(k, cols, -1, 1, O.pair_seed(12))
+        t0 = time.perf_counter()
+        O.corrected3(a, b, variant, block_k=bk, nthreads=threads)
+        dt = time.perf_counter() - t0
+        if fixed or dt >= 0.5 * seconds or rows >= 16384:
+            break
+        grow = min(16.0, max(2.0, seconds / max(dt, 1e-3)))
+        rows = min(16384, int(rows * grow) // threads * threads or threads)
     flops = 2.0 * rows * cols * k
     return {"value": flops / dt / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "port",
             "sample": f"oracle corrected3 ({variant}) on a {rows}x{cols} output block at k={k} "
                       f"({dt:.1f} s); full reference algorithm per output",
-            "seconds": dt}
+            "seconds": dt, "rows": rows}
 
 
 def run_reference(args):
@@ -159,8 +171,10 @@ def run_reference(args):
     vals = []
     sample = None
     steps_s = max(1.0, 60.0 / max(1, args.steps + args.warmup))
+    rows = None
     for i in range(args.warmup + args.steps):
-        r = cpu_oracle_sample(args.variant, args.n, steps_s, threads)
+        r = cpu_oracle_sample(args.variant, args.n, steps_s, threads, rows)
+        rows = r["rows"]
         if i >= args.warmup:
             vals.append(r["value"])
             sample = r
@@ -236,12 +250,14 @@ def main():
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     barrier()
+    w0 = time.time()
     ev0.record(stream)
     for _ in range(args.steps):
         step()
     ev1.record(stream)
     barrier()
-    clk = clocks.stop()
+    w1 = time.time()
+    clk = clocks.stop(window=(w0, w1))
     launches = Nat.launch_count() - launches0
     ms = ev0.elapsed_time(ev1) / args.steps
     t = torch.tensor([ms], device=dev)
@@ -264,8 +280,10 @@ def main():
             traffic = entry.get("dram_bytes_per_launch")
     except Exception:
         pass
+    sustained = float(peaks.get("bf16_tflops_sustained", bf16)) * (1.0 if args.variant == "fp16" else 0.5)
     roofline = {"bound": "tensor", "achieved": eff, "peak": dense / 3.0, "unit": "TFLOP/s",
                 "frac": eff / (dense / 3.0), "traffic": traffic,
+                "frac_vs_sustained_peak": eff / (sustained / 3.0),
                 "peak_basis": f"{'FP16' if args.variant == 'fp16' else 'TF32'} dense / 3 products; "
                               f"dense = {peak_basis} bf16 burst {bf16:.1f} TF/s"
                               + ("" if args.variant == "fp16" else " / 2 (TF32 rate)"),
@@ -348,6 +366,17 @@ def main():
         torch.cuda.synchronize()
         ms_o = e0.elapsed_time(e1) / max(3, args.steps // 2)
         extras[f"{other}_tcec_tflops"] = flops_step / (ms_o * 1e-3) / 1e12
+        # split-once mode (separate split pass + three-product GEMM; opt-in)
+        for v in ("tf32", "fp16"):
+            for _ in range(2):
+                T.gemm_device(A, B, SCHEME[v], out=C, split_mode=2)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for _ in range(3):
+                T.gemm_device(A, B, SCHEME[v], out=C, split_mode=2)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            extras[f"{v}_tcec_split_once_tflops"] = flops_step / (e0.elapsed_time(e1) / 3 * 1e-3) / 1e12
         line["extras"] = extras
         del Cs, ref
 
@@ -386,6 +415,7 @@ def main():
         line["cpu_baseline"] = cpu_oracle_sample(args.variant, n, args.cpu_sample_seconds,
                                                  os.cpu_count() or 1)
         line["cpu_baseline"].pop("seconds", None)
+        line["cpu_baseline"].pop("rows", None)
 
     if rank == 0:
         ex = line.get("extras", {})
