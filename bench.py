@@ -54,6 +54,8 @@ def parse():
     p.add_argument("--variant", choices=["tf32", "fp16"], default="tf32")
     p.add_argument("--n", type=int, default=16384)
     p.add_argument("--allgather", action="store_true")
+    p.add_argument("--overlap-chunks", type=int, default=1,
+                   help="with --allgather: all-gather row chunks while the next chunk computes")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-extras", action="store_true", help="skip cuBLAS / accuracy / other variant")
@@ -230,7 +232,13 @@ def main():
     stream = torch.cuda.current_stream(dev)
     flops_step = 2.0 * n * n * n  # per rank
 
+    from paper_2203_03341_b200.sharded import sharded_gemm
+
     def step():
+        if Cfull is not None and args.overlap_chunks > 1:
+            sharded_gemm(A, B, scheme, m_total=n * world, allgather=True,
+                         overlap_chunks=args.overlap_chunks)
+            return
         T.gemm_device(A, B, scheme, out=C)
         if Cfull is not None:
             dist.all_gather_into_tensor(Cfull, C)

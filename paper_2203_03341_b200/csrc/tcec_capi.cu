@@ -325,9 +325,6 @@ int dispatch_bn(int bn, int64_t m, int64_t n, int64_t k, const float* A, int64_t
       if (kv != 0) return TCEC_ERR_UNSUPPORTED;
       return launch_gemm_ts<V, R, 192, 2>(m, n, k, A, lda, B, ldb, C, ldc, s, de,
                                            gm / 2 > 0 ? gm / 2 : 1, fl, st);
-    case 129:  // measurement: A-from-TMEM kernel at N = 128 with a 4-stage ring
-      return launch_gemm_ts<V, R, 128, 4>(m, n, k, A, lda, B, ldb, C, ldc, s, de,
-                                          gm / 2 > 0 ? gm / 2 : 1, fl, st);
     case 128:
       return launch_gemm<V, R, 128>(m, n, k, A, lda, B, ldb, C, ldc, s, de, gm, fl, st);
     default:
@@ -413,7 +410,7 @@ int tcec_sgemm(int variant, int64_t m, int64_t n, int64_t k, const float* A, int
     drain_every = o.drain_k / bk_op;
   }
   const int block_n = o.block_n == 0 ? 256 : o.block_n;
-  if (block_n != 128 && block_n != 129 && block_n != 192 && block_n != 256) return TCEC_ERR_UNSUPPORTED;
+  if (block_n != 128 && block_n != 192 && block_n != 256) return TCEC_ERR_UNSUPPORTED;
   const int group_m = o.group_m <= 0 ? 8 : o.group_m;
   // reserved[0]: L2 prefetch distance in 32-deep k-slices (pair kernel; 0 = off)
   const int prefetch = o.reserved[0] < 0 ? 0 : (o.reserved[0] > 16 ? 16 : o.reserved[0]);

@@ -29,7 +29,7 @@ def row_slab(m: int, rank: int, world: int) -> tuple[int, int]:
 
 def sharded_gemm(a_slab, b, scheme="corrected3_halfhalf", *, m_total: Optional[int] = None,
                  allgather: bool = False, group=None, out=None,
-                 compute: Optional[Callable] = None):
+                 compute: Optional[Callable] = None, overlap_chunks: int = 1):
     """C_slab = A_slab @ B on this rank; optionally all-gather the full C.
 
     a_slab: this rank's rows of A (rows row_slab(m_total, rank, world)), b: the
@@ -37,6 +37,12 @@ def sharded_gemm(a_slab, b, scheme="corrected3_halfhalf", *, m_total: Optional[i
     `allgather`.  `compute(a, b, scheme)` defaults to the sm_100a kernel
     (gemm_device); tests may substitute the CPU oracle to exercise the
     partition / gather logic on gloo without a GPU.
+
+    overlap_chunks > 1 (with allgather): the slab is computed in that many row
+    chunks (multiples of the 256-row pair tile) and chunk i is all-gathered on
+    a communication stream while chunk i + 1 computes; the gathered rows land
+    directly in their final place (each rank's chunk i is a contiguous row
+    block of the full C).  Same result, bit for bit.
     """
     import torch
     import torch.distributed as dist
@@ -49,6 +55,9 @@ def sharded_gemm(a_slab, b, scheme="corrected3_halfhalf", *, m_total: Optional[i
         def compute(a, bb, sch):
             return gemm_device(a, bb, sch)
 
+    if allgather and world > 1 and overlap_chunks > 1:
+        return _gather_overlapped(a_slab, b, scheme, m_total, world, group, out, compute,
+                                  overlap_chunks)
     c_slab = compute(a_slab, b, scheme)
     if not allgather or world == 1:
         return c_slab
@@ -62,6 +71,53 @@ def sharded_gemm(a_slab, b, scheme="corrected3_halfhalf", *, m_total: Optional[i
         padded[: c_slab.shape[0]].copy_(c_slab)
     full = torch.empty((per * world, n), dtype=c_slab.dtype, device=c_slab.device)
     dist.all_gather_into_tensor(full, padded, group=group)
+    result = full[:m_total]
+    if out is not None:
+        out.copy_(result)
+        return out
+    return result
+
+
+def _gather_overlapped(a_slab, b, scheme, m_total, world, group, out, compute, chunks):
+    import torch
+    import torch.distributed as dist
+
+    if m_total is None:
+        raise ValueError("m_total is required for the all-gather")
+    per = -(-m_total // world)
+    n = b.shape[1]
+    ch = max(1, -(-per // chunks))
+    if ch >= 256:  # whole 256-row pair tiles per chunk
+        ch = -(-ch // 256) * 256
+    full = torch.empty((per * world, n), dtype=b.dtype, device=b.device)
+    cuda = full.is_cuda
+    comm = torch.cuda.Stream(device=full.device) if cuda else None
+    main = torch.cuda.current_stream(full.device) if cuda else None
+    pending = []
+    for r0 in range(0, per, ch):
+        rows = min(ch, per - r0)
+        valid = max(0, min(rows, a_slab.shape[0] - r0))
+        if valid == rows:
+            c = compute(a_slab[r0:r0 + rows], b, scheme)
+        else:  # short last slab: pad with zero rows
+            c = torch.zeros((rows, n), dtype=b.dtype, device=b.device)
+            if valid > 0:
+                c[:valid].copy_(compute(a_slab[r0:r0 + valid], b, scheme))
+        c = c.contiguous()
+        views = [full[r * per + r0: r * per + r0 + rows] for r in range(world)]
+        if cuda:
+            ev = torch.cuda.Event()
+            ev.record(main)
+            comm.wait_event(ev)
+            c.record_stream(comm)
+            with torch.cuda.stream(comm):
+                pending.append(dist.all_gather(views, c, group=group, async_op=True))
+        else:
+            dist.all_gather(views, c, group=group)
+    for w in pending:
+        w.wait()
+    if cuda:
+        main.wait_stream(comm)
     result = full[:m_total]
     if out is not None:
         out.copy_(result)

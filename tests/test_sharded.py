@@ -54,6 +54,9 @@ def _worker(rank, world, port, m, n, k, scheme, q):
         full = sharded_gemm(a[r0:r1], b, scheme, m_total=m, allgather=True,
                             compute=_oracle_compute)
         slab = sharded_gemm(a[r0:r1], b, scheme, compute=_oracle_compute)
+        full3 = sharded_gemm(a[r0:r1], b, scheme, m_total=m, allgather=True,
+                             compute=_oracle_compute, overlap_chunks=3)
+        assert torch.equal(full3, full)  # chunked all-gather: same rows, same places
         if rank == 0:
             q.put((full.numpy().copy(), r0, r1, slab.numpy().copy()))
         dist.barrier()
