@@ -122,6 +122,19 @@ int tcec_sgemm_host(int variant, int64_t m, int64_t n, int64_t k, const float* A
 int tcec_split(int variant, int rounding, int scale_log2, const float* X, int64_t count,
                float* hi, float* lo, uint32_t* d_flags, void* stream);
 
+/* Exhaustive split census over all 2^23 FP32 mantissas (one thread each),
+ * added into d_counts (device, 24 x uint64, caller-zeroed):
+ *   TCEC_CENSUS_KEPT_LENGTH: histogram of the kept mantissa length of the
+ *     markidis_halfhalf split at e_v = 0 with `rounding` (RN / RNA / RZ) --
+ *     analysis.py:138-165 exhaustive_length_distribution (split-stats);
+ *   TCEC_CENSUS_UNDERFLOW: counts[0] = residuals below the FP16 subnormals,
+ *     counts[1] = residuals below the FP16 normals, for inputs of exponent e_v
+ *     split with FP16 RZ -- the exhaustive form of analysis.py:106-135
+ *     empirical_underflow (underflow). */
+#define TCEC_CENSUS_KEPT_LENGTH 0
+#define TCEC_CENSUS_UNDERFLOW 1
+int tcec_split_census(int kind, int rounding, int e_v, unsigned long long* d_counts, void* stream);
+
 /* Number of kernel launches issued by this library since load (diagnostic). */
 uint64_t tcec_launch_count(void);
 

@@ -29,6 +29,7 @@ EXPORTS = (
     "tcec_sgemm",
     "tcec_sgemm_host",
     "tcec_split",
+    "tcec_split_census",
     "tcec_launch_count",
 )
 
@@ -80,6 +81,8 @@ def lib() -> ctypes.CDLL:
     L.tcec_sgemm.argtypes = [i32, i64, i64, i64, p, i64, p, i64, p, i64, p, p, p]
     L.tcec_sgemm_host.restype = i32
     L.tcec_sgemm_host.argtypes = [i32, i64, i64, i64, p, i64, p, i64, p, i64, p, p, p]
+    L.tcec_split_census.restype = i32
+    L.tcec_split_census.argtypes = [i32, i32, i32, p, p]
     L.tcec_split.restype = i32
     L.tcec_split.argtypes = [i32, i32, i32, p, i64, p, p, p, p]
     L.tcec_launch_count.restype = u64

@@ -197,6 +197,50 @@ def rounding_ablation(ms, ns, ks, dist, seeds, block_k: int = 16) -> list[str]:
     return lines
 
 
+def _dyadic_decimal(fr) -> str:
+    """cli.py:42-51: exact decimal of a rational with a power-of-two denominator."""
+    num, den = fr.numerator, fr.denominator
+    k = den.bit_length() - 1
+    if den != 1 << k:
+        raise ValueError(f"denominator {den} is not a power of two")
+    if k == 0:
+        return str(num)
+    digits = str(num * 5 ** k).rjust(k + 1, "0")
+    return digits[:-k] + "." + digits[-k:]
+
+
+def split_stats(rounding: str) -> list[str]:
+    """cmd_split_stats (cli.py:109-117), the enumeration on the GPU."""
+    from .analysis import exhaustive_length_distribution
+
+    if rounding.lower() not in ("rn", "rna", "rz"):
+        raise ValueError(f"unknown rounding mode: {rounding!r}")
+    dist = exhaustive_length_distribution(rounding.lower())
+    lines = ["length,prob_num,prob_den"]
+    for length in sorted(dist.probabilities):
+        p = dist.probabilities[length]
+        lines.append(f"{length},{p.numerator},{p.denominator}")
+    lines.append(f"expectation,{_dyadic_decimal(dist.expectation)}")
+    return lines
+
+
+def underflow(e_min: int, e_max: int) -> list[str]:
+    """cmd_underflow (cli.py:120-132) with the empirical columns computed
+    exhaustively on the GPU (all 2^23 mantissas per exponent) instead of by
+    Monte Carlo sampling."""
+    from .analysis import exhaustive_underflow, gradual_underflow_probability, underflow_probability
+
+    if e_min > e_max:
+        raise ValueError("--e-min must not exceed --e-max")
+    lines = ["e_v,p_u_theory,p_ugu_theory,p_u_emp,p_ugu_emp,samples"]
+    for e_v in range(e_min, e_max + 1):
+        r_u, r_ugu = exhaustive_underflow(e_v)
+        lines.append(f"{e_v},{_dyadic_decimal(underflow_probability(e_v))},"
+                     f"{_dyadic_decimal(gradual_underflow_probability(e_v))},"
+                     f"{_fmt64(float(r_u))},{_fmt64(float(r_ugu))},{1 << 23}")
+    return lines
+
+
 def _add_size_flags(p, default_k: str) -> None:
     p.add_argument("--m", default="16")
     p.add_argument("--n", default="16")
@@ -220,6 +264,11 @@ def _build_parser() -> argparse.ArgumentParser:
     p = sub.add_parser("ablate-delta", help="three-term vs four-term correction")
     _add_size_flags(p, "16,1024")
     p.add_argument("--dist", default="urand:-1,1")
+    p = sub.add_parser("split-stats", help="exact kept-mantissa-length distribution (GPU enumeration)")
+    p.add_argument("--rounding", default="rn", help="rn, rna, or rz")
+    p = sub.add_parser("underflow", help="residual underflow probabilities (theory + GPU enumeration)")
+    p.add_argument("--e-min", type=int, default=-30)
+    p.add_argument("--e-max", type=int, default=14)
     return parser
 
 
@@ -227,8 +276,15 @@ def main(argv: list[str] | None = None) -> int:
     """cli.py:268-281: CSV to stdout or --out; ValueError -> 'error: ...', exit 1."""
     args = _build_parser().parse_args(argv)
     try:
-        sizes = (_parse_int_list(args.m), _parse_int_list(args.n), _parse_int_list(args.k))
-        if args.command == "gemm-accuracy":
+        if args.command == "split-stats":
+            lines = split_stats(args.rounding)
+        elif args.command == "underflow":
+            lines = underflow(args.e_min, args.e_max)
+        else:
+            sizes = (_parse_int_list(args.m), _parse_int_list(args.n), _parse_int_list(args.k))
+        if args.command in ("split-stats", "underflow"):
+            pass
+        elif args.command == "gemm-accuracy":
             lines = gemm_accuracy(*sizes, [s.strip() for s in args.scheme.split(",") if s.strip()],
                                   parse_dist(args.dist), _parse_int_list(args.seeds), args.block_k)
         elif args.command == "ablate-delta":

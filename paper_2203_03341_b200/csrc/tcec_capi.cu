@@ -19,6 +19,7 @@
 #include "tcec_gemm3.cuh"
 #include "tcec_gemm4.cuh"
 #include "tcec_presplit.cuh"
+#include "tcec_census.cuh"
 
 namespace {
 
@@ -550,6 +551,31 @@ int tcec_sgemm_host(int variant, int64_t m, int64_t n, int64_t k, const float* A
   if (s_in) cudaStreamDestroy(s_in);
   if (s_out) cudaStreamDestroy(s_out);
   return status;
+}
+
+int tcec_split_census(int kind, int rounding, int e_v, unsigned long long* d_counts,
+                      void* stream) {
+  if (kind != TCEC_CENSUS_KEPT_LENGTH && kind != TCEC_CENSUS_UNDERFLOW) return TCEC_ERR_ARG;
+  if (d_counts == nullptr) return TCEC_ERR_ARG;
+  if (rounding == TCEC_ROUND_DEFAULT) rounding = TCEC_ROUND_RN;
+  if (rounding != TCEC_ROUND_RN && rounding != TCEC_ROUND_RNA && rounding != TCEC_ROUND_RZ)
+    return TCEC_ERR_ARG;
+  if (kind == TCEC_CENSUS_KEPT_LENGTH && e_v != 0) return TCEC_ERR_UNSUPPORTED;
+  if (e_v < -126 || e_v > 127) return TCEC_ERR_ARG;
+  int s;
+  if ((s = check_arch())) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const unsigned grid = (1u << 23) / 256u;
+  if (kind == TCEC_CENSUS_UNDERFLOW)
+    tcec::tcec_census_kernel<1, tcec::kRZ><<<grid, 256, 0, st>>>(e_v, d_counts);
+  else if (rounding == TCEC_ROUND_RN)
+    tcec::tcec_census_kernel<0, tcec::kRN><<<grid, 256, 0, st>>>(0, d_counts);
+  else if (rounding == TCEC_ROUND_RNA)
+    tcec::tcec_census_kernel<0, tcec::kRNA><<<grid, 256, 0, st>>>(0, d_counts);
+  else
+    tcec::tcec_census_kernel<0, tcec::kRZ><<<grid, 256, 0, st>>>(0, d_counts);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError() == cudaSuccess ? TCEC_OK : TCEC_ERR_CUDA;
 }
 
 int tcec_split(int variant, int rounding, int scale_log2, const float* X, int64_t count,

@@ -210,7 +210,24 @@ def inunit_goldens():
     np.savez_compressed(os.path.join(OUT, "inunit_golden.npz"), **out)
 
 
+def split_stats_goldens():
+    """analysis.py exhaustive_length_distribution (split-stats) for RN / RNA / RZ."""
+    import json
+
+    from tcgemm.analysis import exhaustive_length_distribution
+
+    out = {}
+    for r in ("rn", "rna", "rz"):
+        d = exhaustive_length_distribution(RoundingMode.parse(r))
+        out[r] = {str(k): [v.numerator, v.denominator] for k, v in d.probabilities.items()}
+    with open(os.path.join(OUT, "split_stats_golden.json"), "w") as f:
+        json.dump(out, f, indent=0)
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["split-stats"]:
+        split_stats_goldens()
+        sys.exit(0)
     if sys.argv[1:] == ["inunit"]:
         inunit_goldens()
         sys.exit(0)
@@ -218,4 +235,5 @@ if __name__ == "__main__":
     generator_goldens()
     gemm_goldens()
     inunit_goldens()
+    split_stats_goldens()
     print("wrote", sorted(f for f in os.listdir(OUT) if f.endswith(".npz")))

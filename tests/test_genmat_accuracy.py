@@ -101,3 +101,41 @@ def test_ablation_csvs_on_gpu(tmp_path):
     avg = {ln.split(",")[3]: float(ln.split(",")[5])
            for ln in out.read_text().splitlines() if ",avg," in ln}
     assert avg["tc_plain_fp16"] > 1e-4 and avg["markidis4"] < 1e-4
+
+
+def test_underflow_closed_forms_match_reference_values():
+    """analysis.py closed forms restated (P_u+gu(0) = 1/16,
+    P_u(0) = 0, P_u(-1) = 1/8192)."""
+    from fractions import Fraction
+
+    from paper_2203_03341_b200 import analysis as AN
+
+    assert AN.gradual_underflow_probability(0) == Fraction(1, 16)
+    assert AN.underflow_probability(0) == 0
+    assert AN.underflow_probability(-1) == Fraction(1, 8192)
+    assert sum(AN.zero_run_probability(n) for n in range(14)) == 1
+    assert ACC._dyadic_decimal(Fraction(91, 4)) == "22.75"
+
+
+@pytest.mark.gpu
+def test_split_stats_and_underflow_on_gpu():
+    """GPU enumeration of all 2^23 mantissas equals the reference's
+    exhaustive_length_distribution (tests/golden/split_stats_golden.json, made by
+    the reference) for RN / RNA / RZ, and the exhaustive RZ underflow rates equal
+    the closed forms exactly (the closed forms assume uniform mantissa bits,
+    which the enumeration realises)."""
+    import json
+    import os
+    from fractions import Fraction
+
+    from paper_2203_03341_b200 import analysis as AN
+
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "split_stats_golden.json")))
+    for r, dist in gold.items():
+        got = AN.exhaustive_length_distribution(r).probabilities
+        assert got == {int(k): Fraction(n, d) for k, (n, d) in dist.items()}, r
+    for e_v in range(-30, 15):
+        assert AN.exhaustive_underflow(e_v) == (AN.underflow_probability(e_v),
+                                               AN.gradual_underflow_probability(e_v)), e_v
+    lines = ACC.split_stats("rz")
+    assert lines[-1] == "expectation,22.25"
