@@ -239,8 +239,10 @@ __device__ __forceinline__ void pair_split_loop(uint32_t smem, uint64_t* stg_ful
       sm100::mbar_wait(&stg_full[s], (st / C::NSTG) & 1);
       if (sub == 0) sm100::mbar_wait(&op_empty[o], ((kb / C::NOP) & 1) ^ 1);
       const uint32_t stg = smem + C::OFF_STG + s * C::STG_BYTES;
-      pair_split_part<V, R, kFlags, false>(stg, op, sub, t, scale, fa);
-      pair_split_part<V, R, kFlags, true>(stg, op, sub, t, scale, fa);
+      if (!((TCEC_EXP & 16) && (st & 1))) {
+        pair_split_part<V, R, kFlags, false>(stg, op, sub, t, scale, fa);
+        pair_split_part<V, R, kFlags, true>(stg, op, sub, t, scale, fa);
+      }
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(&stg_empty[s]);
     }
@@ -349,6 +351,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
         sm100::mbar_arrive(&stg_full[s]);
         (void)dst;
 #else
+        if ((TCEC_EXP & 48) && (st & 1)) {
+          sm100::mbar_arrive(&stg_full[s]);
+          continue;
+        }
         sm100::mbar_arrive_expect_tx(&stg_full[s], C::STG_BYTES);
         sm100::tma_load_2d(dst, &tmA, &stg_full[s], st * C::BK_STG, m_cta);
 #pragma unroll
