@@ -301,8 +301,10 @@ def test_reference_scheme_objects_are_accepted():
     c4, _ = _run(a, b, T.corrected3(T.markidis_halfhalf()))
     oc, _ = O.corrected3(a, b, "fp16u", block_k=16, drain_k=128)
     _check_close(c4, oc, a, b, "fp16 unscaled", "fp16u")
-    with pytest.raises(NotImplementedError):
-        T.gemm(a, b, "markidis4")
+    # CPU baselines and the RN-terminal in-unit scheme have no tensor-core form
+    for name in ("corrected4_rn", "fp32_simt", "fp64_ref"):
+        with pytest.raises(NotImplementedError):
+            T.gemm(a, b, name)
 
 
 @pytest.mark.parametrize("sname", ["corrected3_halfhalf", "corrected3_tf32"])
@@ -525,3 +527,23 @@ def test_delta_delta_term_vs_oracle(sname, variant, bk, drain):
     d_gpu = T.relative_residual(r3.output, r4.output)
     d_ref = T.relative_residual(o3, o4)
     assert 0.25 * d_ref <= d_gpu <= 4.0 * d_ref and d_gpu < 1e-6, (d_gpu, d_ref, max_ulp)
+
+
+@pytest.mark.parametrize("name", INUNIT_HW)
+@pytest.mark.parametrize("shape", [(300, 200, 1000), (77, 513, 130), (256, 256, 0)])
+def test_inunit_ragged_vs_oracle(name, shape):
+    """In-unit comparators on ragged shapes (tile edges in m, n and k) against the
+    oracle restatement, with the in-unit tolerance; k = 0 gives zeros."""
+    T = _T()
+    m, n, k = shape
+    a = O.urand(m, k, -1, 1, m + k)
+    b = O.urand(k, n, -1, 1, n + k)
+    run = T.gemm(a, b, _inunit_scheme(T, name))
+    if k == 0:
+        assert np.all(run.output == 0.0)
+        return
+    ref, fl = O.inunit(a, b, name)
+    assert (run.flags.saw_overflow, run.flags.saw_out_of_range) == (bool(fl & 1), bool(fl & 2))
+    mag, terms = _inunit_mag(a, b, name)
+    bound = (terms * (-(-k // 16)) + 2) * 2.0 ** -22 * mag
+    assert np.all(np.abs(run.output.astype(np.float64) - ref) <= bound)
