@@ -74,6 +74,8 @@ if not only or "2" in only:
             ms = timed(lambda: T.gemm_device(A, B, SCH[v], out=C), iters=5 if n <= 8192 else 3)
             out[f"{v}_tcec_tflops"] = 2 * n ** 3 / ms / 1e9
             out[f"{v}_relres"] = relres(C[rows_idx], ref)
+            ms = timed(lambda: T.gemm_device(A, B, SCH[v], out=C, split_mode=2), iters=5 if n <= 8192 else 3)
+            out[f"{v}_tcec_split_once_tflops"] = 2 * n ** 3 / ms / 1e9
         ms = timed(lambda: torch.matmul(A, B, out=C), iters=3)
         out["cublas_sgemm_tflops"] = 2 * n ** 3 / ms / 1e9
         out["cublas_sgemm_relres"] = relres(C[rows_idx], ref)
@@ -120,6 +122,8 @@ if not only or "4" in only:
             ms = timed(lambda: T.gemm_device(A, B, SCH[v], out=C))
             out[f"{v}_tcec_tflops"] = 2 * m * n * k / ms / 1e9
             out[f"{v}_relres"] = relres(C[rows_idx], ref)
+            ms = timed(lambda: T.gemm_device(A, B, SCH[v], out=C, split_mode=2))
+            out[f"{v}_tcec_split_once_tflops"] = 2 * m * n * k / ms / 1e9
         ms = timed(lambda: torch.matmul(A, B, out=C))
         out["cublas_sgemm_tflops"] = 2 * m * n * k / ms / 1e9
         out["cublas_sgemm_relres"] = relres(C[rows_idx], ref)
@@ -138,6 +142,8 @@ if not only or "5" in only:
     for v in ("tf32", "fp16"):
         ms = timed(lambda: T.gemm_device(A, B, SCH[v], out=C), iters=1, warm=1)
         out[f"{v}_tcec_tflops"] = 2 * n ** 3 / ms / 1e9
+        ms = timed(lambda: T.gemm_device(A, B, SCH[v], out=C, split_mode=2), iters=1, warm=1)
+        out[f"{v}_tcec_split_once_tflops"] = 2 * n ** 3 / ms / 1e9
     rows_idx = torch.arange(0, n, n // 64, device=dev)
     ref = A[rows_idx].double() @ B.double()
     out["fp16_relres_64rows"] = relres(C[rows_idx], ref)
