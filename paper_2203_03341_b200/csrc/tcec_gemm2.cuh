@@ -172,12 +172,17 @@ __device__ __forceinline__ void pair_split_part(uint32_t stg, uint32_t op, int s
     row = t & 31;  // k within the slice
     const int qn = t >> 5;
     const uint32_t box = stg + C::STG_A_BYTES + (qn >> 1) * C::STG_B_BOX;
+    // TF32: lanes 4-7 of every 8-lane phase take their four 16-byte chunks in
+    // the order 1,0,3,2 (same data, same registers) so that each STS.128 phase
+    // covers both chunk parities of the SW128_BASE32B rows -- conflict-free
+    // instead of 2-way (ncu: 1.07e9 excess wavefronts per 16384^3 launch).
+    const int h = V == kTF32 ? (t >> 2) & 1 : 0;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
 #if TCEC_EXP & 8
       const float4 v = make_float4(__int_as_float(t * 5 + i), 0.5f + i, 3.5f, -1.25f * qn);
 #else
-      const float4 v = sm100::lds128(box + sw128(row, (qn & 1) * 4 + i));
+      const float4 v = sm100::lds128(box + sw128(row, (qn & 1) * 4 + (i ^ h)));
 #endif
       x[4 * i] = v.x; x[4 * i + 1] = v.y; x[4 * i + 2] = v.z; x[4 * i + 3] = v.w;
     }
@@ -208,9 +213,10 @@ __device__ __forceinline__ void pair_split_part(uint32_t stg, uint32_t op, int s
     const int kop = sub * 32 + row;  // k within the operand stage
     const int grp = kop / C::B_ROWS, rr = kop % C::B_ROWS;
     const uint32_t base = grp * C::B_SBO + (((t >> 5) * 16) / C::B_ATOM_N) * C::B_LBO + rr * 128;
+    const int h = V == kTF32 ? (t >> 2) & 1 : 0;  // chunk order, see the loads above
 #pragma unroll
     for (int q = 0; q < NCH; ++q) {
-      const int c16 = chunk_first + q;
+      const int c16 = chunk_first + (q ^ h);
       // FP16 SW128: 16-byte chunk ^ row; TF32 SW128_BASE32B: 32-byte chunk ^ (row & 3)
       const uint32_t off = V == kFP16 ? base + ((c16 ^ rr) << 4)
                                       : base + ((((c16 >> 1) ^ rr) & 3) << 5) + ((c16 & 1) << 4);

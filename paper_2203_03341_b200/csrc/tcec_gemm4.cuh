@@ -116,10 +116,11 @@ __device__ __forceinline__ void ts_split_slice(uint32_t stg, uint32_t op, uint32
   if (t < 32 * 2 * C::NUM_B_BOXES) {
     const int row = t & 31, qn = t >> 5;
     const uint32_t box = stg + C::STG_A_BYTES + (qn >> 1) * C::STG_B_BOX;
+    const int h = V == kTF32 ? (t >> 2) & 1 : 0;  // TF32 chunk order (conflict-free STS)
     float x[16];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const float4 v = sm100::lds128(box + sw128(row, (qn & 1) * 4 + i));
+      const float4 v = sm100::lds128(box + sw128(row, (qn & 1) * 4 + (i ^ h)));
       x[4 * i] = v.x; x[4 * i + 1] = v.y; x[4 * i + 2] = v.z; x[4 * i + 3] = v.w;
     }
     if constexpr (kFlags) {
@@ -145,7 +146,7 @@ __device__ __forceinline__ void ts_split_slice(uint32_t stg, uint32_t op, uint32
       // SW128_BASE32B (Swizzle<2,5,2>): 32-byte chunk ^ (row & 3); 16 n = 16-byte chunks 4 (qn & 1) + q
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const int c16 = (qn & 1) * 4 + q;
+        const int c16 = (qn & 1) * 4 + (q ^ h);
         const uint32_t off = base + ((((c16 >> 1) ^ rr) & 3) << 5) + ((c16 & 1) << 4);
         sm100::sts128(hi_base + off, hw[4 * q], hw[4 * q + 1], hw[4 * q + 2], hw[4 * q + 3]);
         sm100::sts128(lo_base + off, lw[4 * q], lw[4 * q + 1], lw[4 * q + 2], lw[4 * q + 3]);
