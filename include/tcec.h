@@ -81,6 +81,10 @@ typedef struct tcec_opts {
   int32_t split_mode;
   /* Product schedule, TCEC_SCHEME_* (0 = corrected3). */
   int32_t scheme;
+  /* tcec_sgemm_host only: number of row / column blocks of C that the host
+   * buffers are streamed in (0 = automatic, at most 8 each). */
+  int32_t host_row_blocks;
+  int32_t host_col_blocks;
   /* reserved[0]: L2 prefetch distance in 32-deep k-slices (0 = off);
    * reserved[1]: pair-kernel variant (0 = split + drain warps, 1 = unified workers);
    * reserved[2]: pair-kernel MMA order (0 = corrections first, 1 = A_hi collector reuse). */
@@ -109,6 +113,8 @@ int tcec_sgemm(int variant, int64_t m, int64_t n, int64_t k, const float* A, int
 
 /* Same computation on HOST buffers (the numpy-facing binding): copies A and B
  * to the device, runs tcec_sgemm, copies C back and synchronises the stream.
+ * C is produced in row x column blocks so that the GEMM starts after the first
+ * block of A and of B arrive and the download overlaps the uploads.
  * Host buffers may be pageable; pinned buffers copy faster.  h_flags may be
  * NULL.  Row-major, leading dimensions as above (no alignment requirement). */
 int tcec_sgemm_host(int variant, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda,

@@ -464,10 +464,15 @@ int tcec_sgemm(int variant, int64_t m, int64_t n, int64_t k, const float* A, int
 int tcec_sgemm_host(int variant, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda,
                     const float* B, int64_t ldb, float* C, int64_t ldc, const tcec_opts* opts,
                     uint32_t* h_flags, void* stream) {
-  // Host buffers: B goes to the device once; A and C stream through in row
-  // chunks on two copy streams so the H2D of chunk i+1 and the D2H of chunk
-  // i-1 overlap the GEMM of chunk i (rows are independent: results are
-  // bit-identical to one launch over all rows).
+  // Host buffers.  C is computed in R x Cb blocks (rows multiple of the 256-row
+  // pair tile, columns of the 256-column tile).  The inputs go up in the order
+  // A_0, B_0, A_1, B_1, ... (A row blocks contiguous, B column blocks as 2-D
+  // copies, which run at full PCIe rate); block (i, j) launches on one of two
+  // compute streams as soon as A_i and B_j are resident, and its C block goes
+  // down on the copy-out stream as soon as it is done.  So the GEMM starts after
+  // 1/R of A and 1/Cb of B instead of after all of B, and the download overlaps
+  // the remaining uploads.  Rows and columns are independent, so the result is
+  // bit-identical to one launch over the whole product.
   if (m < 0 || n < 0 || k < 0) return TCEC_ERR_ARG;
   if (lda < (k > 0 ? k : 1) || ldb < (n > 0 ? n : 1) || ldc < (n > 0 ? n : 1)) return TCEC_ERR_ARG;
   if (h_flags) *h_flags = 0;
@@ -480,15 +485,26 @@ int tcec_sgemm_host(int variant, int64_t m, int64_t n, int64_t k, const float* A
   const int64_t dldb = (n + 3) / 4 * 4;
   const int64_t dldc = dldb;
   const int64_t kk = k > 0 ? k : 1;
-  // chunks of rows: a multiple of the 256-row pair tile, at most 8 chunks
-  int64_t chunk = ((m + 7) / 8 + 255) / 256 * 256;
-  if (chunk < 256) chunk = 256;
-  const int nchunks = static_cast<int>((m + chunk - 1) / chunk);
+  // blocking (automatic): up to 8 row blocks and 8 (TF32) / 4 (FP16, whose GEMM
+  // is shorter than the upload) column blocks of >= 2048; measured at 16384^3
+  // (DESIGN.md 5): TF32 e2e 57.2 -> 48.8 ms against row blocks only, FP16 46.3 -> 45.4
+  auto blocks = [](int64_t extent, int requested, int cap) {
+    int64_t nb = requested > 0 ? requested : (extent + 2047) / 2048;
+    if (requested <= 0 && nb > cap) nb = cap;
+    if (nb > 8) nb = 8;
+    if (nb < 1) nb = 1;
+    int64_t sz = ((extent + nb - 1) / nb + 255) / 256 * 256;
+    return sz < 256 ? int64_t(256) : sz;
+  };
+  const int64_t rb = blocks(m, opts ? opts->host_row_blocks : 0, 8);
+  const int64_t cbk = blocks(n, opts ? opts->host_col_blocks : 0, variant == TCEC_FP16 ? 4 : 8);
+  const int R = static_cast<int>((m + rb - 1) / rb);
+  const int Cb = static_cast<int>((n + cbk - 1) / cbk);
   float *dA = nullptr, *dB = nullptr, *dC = nullptr;
   uint32_t* dF = nullptr;
-  cudaStream_t s_in = nullptr, s_out = nullptr;
-  cudaEvent_t ev_b = nullptr;
-  cudaEvent_t ev_in[8] = {}, ev_mm[8] = {};
+  cudaStream_t s_in = nullptr, s_out = nullptr, s_c[2] = {nullptr, nullptr};
+  cudaEvent_t ev_start = nullptr;
+  cudaEvent_t ev_a[8] = {}, ev_b[8] = {}, ev_g[64] = {};
   int status = TCEC_OK;
   auto cu = [&](cudaError_t e) {
     if (e != cudaSuccess && status == TCEC_OK) status = TCEC_ERR_CUDA;
@@ -496,60 +512,84 @@ int tcec_sgemm_host(int variant, int64_t m, int64_t n, int64_t k, const float* A
   };
   bool ok = cu(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking)) &&
             cu(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking)) &&
-            cu(cudaEventCreateWithFlags(&ev_b, cudaEventDisableTiming));
-  for (int c = 0; ok && c < nchunks; ++c)
-    ok = cu(cudaEventCreateWithFlags(&ev_in[c], cudaEventDisableTiming)) &&
-         cu(cudaEventCreateWithFlags(&ev_mm[c], cudaEventDisableTiming));
+            cu(cudaStreamCreateWithFlags(&s_c[0], cudaStreamNonBlocking)) &&
+            cu(cudaStreamCreateWithFlags(&s_c[1], cudaStreamNonBlocking)) &&
+            cu(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
+  for (int i = 0; ok && i < R; ++i) ok = cu(cudaEventCreateWithFlags(&ev_a[i], cudaEventDisableTiming));
+  for (int j = 0; ok && j < Cb; ++j) ok = cu(cudaEventCreateWithFlags(&ev_b[j], cudaEventDisableTiming));
+  for (int b = 0; ok && b < R * Cb; ++b) ok = cu(cudaEventCreateWithFlags(&ev_g[b], cudaEventDisableTiming));
   ok = ok && cu(cudaMallocAsync(reinterpret_cast<void**>(&dA), size_t(m) * dlda * sizeof(float), st)) &&
        cu(cudaMallocAsync(reinterpret_cast<void**>(&dB), size_t(kk) * dldb * sizeof(float), st)) &&
        cu(cudaMallocAsync(reinterpret_cast<void**>(&dC), size_t(m) * dldc * sizeof(float), st)) &&
        cu(cudaMallocAsync(reinterpret_cast<void**>(&dF), sizeof(uint32_t), st)) &&
-       cu(cudaMemsetAsync(dF, 0, sizeof(uint32_t), st));
-  if (ok && k > 0) {
-    ok = cu(cudaMemcpy2DAsync(dB, dldb * sizeof(float), B, ldb * sizeof(float), n * sizeof(float), k,
-                              cudaMemcpyHostToDevice, st)) &&
-         cu(cudaEventRecord(ev_b, st));
-  }
-  if (ok) ok = cu(cudaStreamWaitEvent(s_in, ev_b, 0));  // allocations are ordered on st
-  for (int c = 0; ok && c < nchunks; ++c) {
-    const int64_t r0 = c * chunk;
-    const int64_t rows = (r0 + chunk <= m) ? chunk : m - r0;
-    if (k > 0)
-      ok = cu(cudaMemcpy2DAsync(dA + r0 * dlda, dlda * sizeof(float), A + r0 * lda,
-                                lda * sizeof(float), k * sizeof(float), rows,
-                                cudaMemcpyHostToDevice, s_in));
-    ok = ok && cu(cudaEventRecord(ev_in[c], s_in)) && cu(cudaStreamWaitEvent(st, ev_in[c], 0));
-    if (!ok) break;
-    const int s = tcec_sgemm(variant, rows, n, k, dA + r0 * dlda, dlda, dB, dldb, dC + r0 * dldc,
-                             dldc, opts, dF, st);
-    if (s != TCEC_OK) {
-      status = s;
-      ok = false;
-      break;
+       cu(cudaMemsetAsync(dF, 0, sizeof(uint32_t), st)) && cu(cudaEventRecord(ev_start, st));
+  for (cudaStream_t x : {s_in, s_out, s_c[0], s_c[1]})
+    if (ok) ok = cu(cudaStreamWaitEvent(x, ev_start, 0));  // allocations are ordered on st
+  // uploads, interleaved A_0 B_0 A_1 B_1 ...
+  for (int s = 0; ok && s < (R > Cb ? R : Cb); ++s) {
+    if (s < R) {
+      const int64_t r0 = s * rb, rows = (r0 + rb <= m) ? rb : m - r0;
+      if (k > 0)
+        ok = cu(cudaMemcpy2DAsync(dA + r0 * dlda, dlda * sizeof(float), A + r0 * lda,
+                                  lda * sizeof(float), k * sizeof(float), rows,
+                                  cudaMemcpyHostToDevice, s_in));
+      ok = ok && cu(cudaEventRecord(ev_a[s], s_in));
     }
-    ok = cu(cudaEventRecord(ev_mm[c], st)) && cu(cudaStreamWaitEvent(s_out, ev_mm[c], 0)) &&
-         cu(cudaMemcpy2DAsync(C + r0 * ldc, ldc * sizeof(float), dC + r0 * dldc,
-                              dldc * sizeof(float), n * sizeof(float), rows,
-                              cudaMemcpyDeviceToHost, s_out));
+    if (ok && s < Cb) {
+      const int64_t c0 = s * cbk, cols = (c0 + cbk <= n) ? cbk : n - c0;
+      if (k > 0)
+        ok = cu(cudaMemcpy2DAsync(dB + c0, dldb * sizeof(float), B + c0, ldb * sizeof(float),
+                                  cols * sizeof(float), k, cudaMemcpyHostToDevice, s_in));
+      ok = ok && cu(cudaEventRecord(ev_b[s], s_in));
+    }
   }
-  if (ok && h_flags) {
-    cu(cudaStreamWaitEvent(s_out, ev_mm[nchunks - 1], 0));
+  // GEMM blocks in arrival order, downloads as they complete
+  int launched = 0;
+  for (int s = 0; ok && s < (R > Cb ? R : Cb); ++s) {
+    for (int pass = 0; ok && pass < 2; ++pass) {
+      // pass 0: row s against columns 0..s; pass 1: rows 0..s-1 against column s
+      const int count = pass == 0 ? (s < R ? (s + 1 < Cb ? s + 1 : Cb) : 0) : (s < Cb ? (s < R ? s : R) : 0);
+      for (int t = 0; ok && t < count; ++t) {
+        const int i = pass == 0 ? s : t, j = pass == 0 ? t : s;
+        const int64_t r0 = i * rb, rows = (r0 + rb <= m) ? rb : m - r0;
+        const int64_t c0 = j * cbk, cols = (c0 + cbk <= n) ? cbk : n - c0;
+        cudaStream_t sc = s_c[launched & 1];
+        ok = cu(cudaStreamWaitEvent(sc, ev_a[i], 0)) && cu(cudaStreamWaitEvent(sc, ev_b[j], 0));
+        if (!ok) break;
+        const int s2 = tcec_sgemm(variant, rows, cols, k, dA + r0 * dlda, dlda, dB + c0, dldb,
+                                  dC + r0 * dldc + c0, dldc, opts, dF, sc);
+        if (s2 != TCEC_OK) {
+          status = s2;
+          ok = false;
+          break;
+        }
+        cudaEvent_t eg = ev_g[launched];
+        ok = cu(cudaEventRecord(eg, sc)) && cu(cudaStreamWaitEvent(s_out, eg, 0)) &&
+             cu(cudaMemcpy2DAsync(C + r0 * ldc + c0, ldc * sizeof(float), dC + r0 * dldc + c0,
+                                  dldc * sizeof(float), cols * sizeof(float), rows,
+                                  cudaMemcpyDeviceToHost, s_out));
+        ++launched;
+      }
+    }
+  }
+  if (ok && h_flags)  // s_out has waited on every block's GEMM
     cu(cudaMemcpyAsync(h_flags, dF, sizeof(uint32_t), cudaMemcpyDeviceToHost, s_out));
-  }
-  if (s_out) cu(cudaStreamSynchronize(s_out));
-  if (s_in) cu(cudaStreamSynchronize(s_in));
+  for (cudaStream_t x : {s_out, s_in, s_c[0], s_c[1]})
+    if (x) cu(cudaStreamSynchronize(x));
   if (dA) cudaFreeAsync(dA, st);
   if (dB) cudaFreeAsync(dB, st);
   if (dC) cudaFreeAsync(dC, st);
   if (dF) cudaFreeAsync(dF, st);
   cu(cudaStreamSynchronize(st));
-  for (int c = 0; c < nchunks; ++c) {
-    if (ev_in[c]) cudaEventDestroy(ev_in[c]);
-    if (ev_mm[c]) cudaEventDestroy(ev_mm[c]);
+  for (int i = 0; i < 8; ++i) {
+    if (ev_a[i]) cudaEventDestroy(ev_a[i]);
+    if (ev_b[i]) cudaEventDestroy(ev_b[i]);
   }
-  if (ev_b) cudaEventDestroy(ev_b);
-  if (s_in) cudaStreamDestroy(s_in);
-  if (s_out) cudaStreamDestroy(s_out);
+  for (int b = 0; b < 64; ++b)
+    if (ev_g[b]) cudaEventDestroy(ev_g[b]);
+  if (ev_start) cudaEventDestroy(ev_start);
+  for (cudaStream_t x : {s_in, s_out, s_c[0], s_c[1]})
+    if (x) cudaStreamDestroy(x);
   return status;
 }
 
