@@ -172,7 +172,8 @@ def run_reference(args):
     threads = os.cpu_count() or 1
     vals = []
     sample = None
-    steps_s = max(1.0, 60.0 / max(1, args.steps + args.warmup))
+    # each step a bounded sample: the whole run stays near a minute of CPU time
+    steps_s = min(args.cpu_sample_seconds, max(1.0, 60.0 / max(1, args.steps + args.warmup)))
     rows = None
     for i in range(args.warmup + args.steps):
         r = cpu_oracle_sample(args.variant, args.n, steps_s, threads, rows)
