@@ -441,6 +441,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
       pair_split_loop<V, R, false>(smem_base, stg_full, stg_empty, op_full, op_empty, nop, t, lane, scale, fa);
     }
   } else {
+    // setmaxnreg can only redistribute the launch allocation (96 x 640 registers):
+    // 4 x 40 + 8 x 56 + 8 x 160 = 1888 <= 20 x 96 = 1920 per lane slot
     sm100::regs_inc<160>();
     // ===================== drain + epilogue =====================
     const int q = warp & 3;
@@ -459,8 +461,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
         sm100::tmem_ld_32x32b_x16(tmem_P + lane_off + h * 128 + c * 16, r);
         sm100::tmem_ld_wait();
 #pragma unroll
-        for (int j = 0; j < 16; ++j)  // schemes.py:300-304: c = RN32(c + partial)
-          acc[c * 16 + j] = __fadd_rn(acc[c * 16 + j], __uint_as_float(r[j]));
+        for (int j = 0; j < 16; j += 2) {  // schemes.py:300-304: c = RN32(c + partial)
+          if constexpr (V == kTF32) {
+            // two RN adds per f32x2 instruction (measured +3% for TF32; the FP16
+            // kernel keeps scalar adds: the register pairs make its drain spill)
+            sm100::fadd2_rn(acc[c * 16 + j], acc[c * 16 + j + 1], __uint_as_float(r[j]),
+                            __uint_as_float(r[j + 1]));
+          } else {
+            acc[c * 16 + j] = __fadd_rn(acc[c * 16 + j], __uint_as_float(r[j]));
+            acc[c * 16 + j + 1] = __fadd_rn(acc[c * 16 + j + 1], __uint_as_float(r[j + 1]));
+          }
+        }
       }
       sm100::tc_fence_before();
       __syncwarp();
