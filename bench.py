@@ -56,6 +56,9 @@ def parse():
     p.add_argument("--allgather", action="store_true")
     p.add_argument("--overlap-chunks", type=int, default=1,
                    help="with --allgather: all-gather row chunks while the next chunk computes")
+    p.add_argument("--fused-allgather", action="store_true",
+                   help="with --allgather: gather C in the GEMM epilogue over symmetric memory "
+                        "(peer TMA stores, no NCCL collective)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-extras", action="store_true", help="skip cuBLAS / accuracy / other variant")
@@ -233,9 +236,12 @@ def main():
     stream = torch.cuda.current_stream(dev)
     flops_step = 2.0 * n * n * n  # per rank
 
-    from paper_2203_03341_b200.sharded import sharded_gemm
+    from paper_2203_03341_b200.sharded import sharded_gemm, sharded_gemm_fused
 
     def step():
+        if Cfull is not None and args.fused_allgather:
+            sharded_gemm_fused(A, B, scheme, m_total=n * world)
+            return
         if Cfull is not None and args.overlap_chunks > 1:
             sharded_gemm(A, B, scheme, m_total=n * world, allgather=True,
                          overlap_chunks=args.overlap_chunks)
@@ -307,7 +313,9 @@ def main():
         "config": {"workload": f"{'TF32' if args.variant == 'tf32' else 'FP16'}-TCEC SGEMM "
                                f"m=n=k={n} per rank" + (", row-sharded" if world > 1 else ""),
                    "variant": args.variant, "scheme": scheme, "m": n * world, "n": n, "k": n,
-                   "parallelism": f"row-shard x{world}" + (" + all-gather C" if Cfull is not None else ""),
+                   "parallelism": f"row-shard x{world}" + (
+                       (" + fused all-gather C (epilogue peer stores)" if args.fused_allgather
+                        else " + all-gather C") if Cfull is not None else ""),
                    "l2": "inputs 1 GiB each > 126 MB L2 (no flush needed)"},
         "clocks": clk, "gpu_launches": int(launches),
         "roofline": roofline,

@@ -111,6 +111,17 @@ int tcec_sgemm(int variant, int64_t m, int64_t n, int64_t k, const float* A, int
                const float* B, int64_t ldb, float* C, int64_t ldc, const tcec_opts* opts,
                uint32_t* d_flags, void* stream);
 
+/* Same computation, with C stored to each of the n_c (1..8) destinations C[0..n_c-1]
+ * (same ldc) by the same TMA-store epilogue -- the fused all-gather of the
+ * row-sharded multi-GPU GEMM: C[d] is this rank's slab inside rank d's full C
+ * (peer memory mapped into this GPU's address space, e.g. CUDA IPC / symmetric
+ * memory over NVLink), so the gather overlaps the GEMM tile by tile and needs no
+ * separate collective.  Default kernel options only (pair kernel, fused split,
+ * corrected3); the caller synchronises the ranks before reading the full C. */
+int tcec_sgemm_multi(int variant, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda,
+                     const float* B, int64_t ldb, float* const* C, int n_c, int64_t ldc,
+                     const tcec_opts* opts, uint32_t* d_flags, void* stream);
+
 /* Same computation on HOST buffers (the numpy-facing binding): copies A and B
  * to the device, runs tcec_sgemm, copies C back and synchronises the stream.
  * C is produced in row x column blocks so that the GEMM starts after the first

@@ -10,7 +10,7 @@ from .analysis import relative_residual
 from .formats import ACC25, FP16, FP32, TF32, FloatFormat, RoundingMode
 from .schemes import (SCHEMES_BY_NAME, GemmKind, GemmRun, GemmScheme, MmaConfig, RunFlags,
                       corrected3, corrected4, default_config, delta_term_ablation, fp32_lsbtrunc,
-                      fp32_simt, fp64_ref, gemm, gemm_device, markidis4, resolve_schedule,
+                      fp32_simt, fp64_ref, gemm, gemm_device, gemm_device_multi, markidis4, resolve_schedule,
                       resolve_scheme, tc_plain)
 from .splitting import (RESIDUAL_SCALE_LOG2, SplitKind, SplitMatrices, SplitScheme,
                         markidis_halfhalf, scaled_halfhalf, split_device, split_matrix, tf32tf32)

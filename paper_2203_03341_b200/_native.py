@@ -28,6 +28,7 @@ EXPORTS = (
     "tcec_status_str",
     "tcec_sgemm",
     "tcec_sgemm_host",
+    "tcec_sgemm_multi",
     "tcec_split",
     "tcec_split_census",
     "tcec_launch_count",
@@ -81,6 +82,8 @@ def lib() -> ctypes.CDLL:
     L.tcec_status_str.argtypes = [i32]
     L.tcec_sgemm.restype = i32
     L.tcec_sgemm.argtypes = [i32, i64, i64, i64, p, i64, p, i64, p, i64, p, p, p]
+    L.tcec_sgemm_multi.restype = i32
+    L.tcec_sgemm_multi.argtypes = [i32, i64, i64, i64, p, i64, p, i64, p, i32, i64, p, p, p]
     L.tcec_sgemm_host.restype = i32
     L.tcec_sgemm_host.argtypes = [i32, i64, i64, i64, p, i64, p, i64, p, i64, p, p, p]
     L.tcec_split_census.restype = i32

@@ -98,6 +98,13 @@ void keep_pool(int dev) {
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+// Extra destinations of C (tcec_sgemm_multi): the pair kernel stores every
+// output box to each of them as well.
+struct ExtraC {
+  float* c[tcec::kMaxExtraC];
+  int count;
+};
+
 template <int V, int R, int BN>
 int launch_gemm(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, const float* B,
                 int64_t ldb, float* C, int64_t ldc, int scale_log2, int drain_every, int group_m,
@@ -143,8 +150,8 @@ int launch_gemm(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, co
 template <int V, int R, bool kUnified>
 int launch_gemm_pair(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, const float* B,
                      int64_t ldb, float* C, int64_t ldc, int scale_log2, int drain_every,
-                     int group_m, int prefetch, int mma_order, uint32_t* d_flags,
-                     cudaStream_t stream) {
+                     int group_m, int prefetch, int mma_order, const ExtraC* ex,
+                     uint32_t* d_flags, cudaStream_t stream) {
   using Cfg = tcec::PairCfg<V>;
   using VC = tcec::VarCfg<V>;
   CUtensorMap tmA, tmB, tmC;
@@ -153,6 +160,12 @@ int launch_gemm_pair(int64_t m, int64_t n, int64_t k, const float* A, int64_t ld
     return st;
   if ((st = make_tmap(&tmB, B, n, k, ldb, 32, Cfg::BK_STG, CU_TENSOR_MAP_SWIZZLE_128B))) return st;
   if ((st = make_tmap(&tmC, C, n, m, ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B))) return st;
+  tcec::CDests cx;
+  memset(&cx, 0, sizeof(cx));
+  cx.count = ex ? ex->count : 0;
+  for (int d = 0; d < cx.count; ++d)
+    if ((st = make_tmap(&cx.m[d], ex->c[d], n, m, ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B)))
+      return st;
 
   auto kern = kUnified ? tcec::tcec_gemm_pair_uni_kernel<V, R> : tcec::tcec_gemm_pair_kernel<V, R>;
   static std::once_flag attr_once;
@@ -177,7 +190,7 @@ int launch_gemm_pair(int64_t m, int64_t n, int64_t k, const float* A, int64_t ld
   const tcec::FlagThresholds thr = tcec::flag_thresholds(V, R, scale_log2);
   const int64_t pairs = ((m + 2 * Cfg::BM - 1) / (2 * Cfg::BM)) * ((n + Cfg::BN - 1) / Cfg::BN);
   kern<<<static_cast<unsigned>(2 * pairs), Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream>>>(
-      tmA, tmB, tmC, shp, scale, inv_scale, thr, d_flags);
+      tmA, tmB, tmC, cx, shp, scale, inv_scale, thr, d_flags);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError() == cudaSuccess ? TCEC_OK : TCEC_ERR_CUDA;
 }
@@ -297,7 +310,10 @@ int launch_gemm_presplit(int64_t m, int64_t n, int64_t k, const float* A, int64_
 template <int V, int R>
 int dispatch_bn(int bn, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda,
                 const float* B, int64_t ldb, float* C, int64_t ldc, int s, int de, int gm, int pf,
-                int kv, int mo, int sm, int sch, uint32_t* fl, cudaStream_t st) {
+                int kv, int mo, int sm, int sch, const ExtraC* ex, uint32_t* fl,
+                cudaStream_t st) {
+  if (ex && ex->count > 0 && (bn != 256 || sm == 2 || sch != TCEC_SCHEME_CORRECTED3))
+    return TCEC_ERR_UNSUPPORTED;  // extra destinations: the default pair kernels only
   if (sm == 2 || sch != TCEC_SCHEME_CORRECTED3) {
     if ((bn != 256 && bn != 0) || kv != 0 || mo != 0) return TCEC_ERR_UNSUPPORTED;
     const int g = gm / 2 > 0 ? gm / 2 : 1;
@@ -318,10 +334,10 @@ int dispatch_bn(int bn, int64_t m, int64_t n, int64_t k, const float* A, int64_t
     case 256:
       if (kv == 1)
         return launch_gemm_pair<V, R, true>(m, n, k, A, lda, B, ldb, C, ldc, s, de,
-                                            gm / 2 > 0 ? gm / 2 : 1, pf, mo, fl, st);
+                                            gm / 2 > 0 ? gm / 2 : 1, pf, mo, ex, fl, st);
       if (kv != 0) return TCEC_ERR_UNSUPPORTED;
       return launch_gemm_pair<V, R, false>(m, n, k, A, lda, B, ldb, C, ldc, s, de,
-                                           gm / 2 > 0 ? gm / 2 : 1, pf, mo, fl, st);
+                                           gm / 2 > 0 ? gm / 2 : 1, pf, mo, ex, fl, st);
     case 192:
       if (kv != 0) return TCEC_ERR_UNSUPPORTED;
       return launch_gemm_ts<V, R, 192, 2>(m, n, k, A, lda, B, ldb, C, ldc, s, de,
@@ -383,9 +399,13 @@ const char* tcec_status_str(int status) {
   }
 }
 
-int tcec_sgemm(int variant, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda,
+}  // extern "C"
+
+namespace {
+
+int sgemm_impl(int variant, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda,
                const float* B, int64_t ldb, float* C, int64_t ldc, const tcec_opts* opts,
-               uint32_t* d_flags, void* stream) {
+               const ExtraC* ex, uint32_t* d_flags, void* stream) {
   if (variant != TCEC_FP16 && variant != TCEC_TF32) return TCEC_ERR_ARG;
   if (m < 0 || n < 0 || k < 0) return TCEC_ERR_ARG;
   if (m > INT32_MAX || n > INT32_MAX || k > INT32_MAX) return TCEC_ERR_ARG;
@@ -443,22 +463,53 @@ int tcec_sgemm(int variant, int64_t m, int64_t n, int64_t k, const float* A, int
   if (variant == TCEC_FP16) {
     if (rounding == TCEC_ROUND_RN)
       return dispatch_bn<tcec::kFP16, tcec::kRN>(block_n, m, n, k, A, lda, B, ldb, C, ldc,
-                                                 scale_log2, drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, d_flags, st);
+                                                 scale_log2, drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, ex, d_flags, st);
     if (rounding == TCEC_ROUND_RZ)
       return dispatch_bn<tcec::kFP16, tcec::kRZ>(block_n, m, n, k, A, lda, B, ldb, C, ldc,
-                                                 scale_log2, drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, d_flags, st);
+                                                 scale_log2, drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, ex, d_flags, st);
     return TCEC_ERR_UNSUPPORTED;
   }
   if (rounding == TCEC_ROUND_RNA)
     return dispatch_bn<tcec::kTF32, tcec::kRNA>(block_n, m, n, k, A, lda, B, ldb, C, ldc, 0,
-                                                drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, d_flags, st);
+                                                drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, ex, d_flags, st);
   if (rounding == TCEC_ROUND_RN)
     return dispatch_bn<tcec::kTF32, tcec::kRN>(block_n, m, n, k, A, lda, B, ldb, C, ldc, 0,
-                                               drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, d_flags, st);
+                                               drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, ex, d_flags, st);
   if (rounding == TCEC_ROUND_RZ)
     return dispatch_bn<tcec::kTF32, tcec::kRZ>(block_n, m, n, k, A, lda, B, ldb, C, ldc, 0,
-                                               drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, d_flags, st);
+                                               drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, ex, d_flags, st);
   return TCEC_ERR_UNSUPPORTED;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tcec_sgemm(int variant, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda,
+               const float* B, int64_t ldb, float* C, int64_t ldc, const tcec_opts* opts,
+               uint32_t* d_flags, void* stream) {
+  return sgemm_impl(variant, m, n, k, A, lda, B, ldb, C, ldc, opts, nullptr, d_flags, stream);
+}
+
+int tcec_sgemm_multi(int variant, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda,
+                     const float* B, int64_t ldb, float* const* C, int n_c, int64_t ldc,
+                     const tcec_opts* opts, uint32_t* d_flags, void* stream) {
+  if (C == nullptr || n_c < 1 || n_c > 1 + tcec::kMaxExtraC) return TCEC_ERR_ARG;
+  ExtraC ex;
+  ex.count = n_c - 1;
+  for (int d = 0; d < ex.count; ++d) {
+    if (C[1 + d] == nullptr || !aligned16(C[1 + d])) return TCEC_ERR_ALIGN;
+    ex.c[d] = C[1 + d];
+  }
+  if (k == 0 && ex.count > 0) {  // zeros into every destination
+    for (int d = 0; d < n_c; ++d) {
+      const int s = sgemm_impl(variant, m, n, 0, A, lda, B, ldb, C[d], ldc, opts, nullptr, d_flags,
+                               stream);
+      if (s != TCEC_OK) return s;
+    }
+    return TCEC_OK;
+  }
+  return sgemm_impl(variant, m, n, k, A, lda, B, ldb, C[0], ldc, opts, &ex, d_flags, stream);
 }
 
 int tcec_sgemm_host(int variant, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda,

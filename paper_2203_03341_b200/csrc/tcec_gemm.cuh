@@ -35,6 +35,15 @@ struct GemmShape {
   int32_t mma_order;       // pair kernel: 1 = A_hi reuse through the MMA collector
 };
 
+// Extra destinations of the output tile (fused all-gather: this rank's C slab
+// stored into every peer's full C over NVLink by the same TMA-store epilogue).
+// Each map covers the same m x n slab (the pointer already offset to it).
+constexpr int kMaxExtraC = 7;
+struct CDests {
+  CUtensorMap m[kMaxExtraC];
+  int32_t count;
+};
+
 template <int BN_>
 struct TileCfg {
   static constexpr int BM = 128;

@@ -266,6 +266,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
     tcec_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA,  // A [m][k], box 32 x 128, SW128
                           const __grid_constant__ CUtensorMap tmB,  // B [k][n], box 32 x 32, SW128
                           const __grid_constant__ CUtensorMap tmC,  // C [m][n], box 32 x 32, SW128
+                          const __grid_constant__ CDests cx,        // extra copies of C (all-gather)
                           const GemmShape shp, const float scale, const float inv_scale,
                           const FlagThresholds thr, uint32_t* __restrict__ flags) {
   using C = PairCfg<V>;
@@ -504,6 +505,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
       __syncwarp();
       if (lane == 0) {
         sm100::tma_store_2d(&tmC, smem + (box - smem_base), n_pair + h * 128 + b * 32, m_cta + q * 32);
+        for (int d = 0; d < cx.count; ++d)  // fused all-gather: the same box to every peer
+          sm100::tma_store_2d(&cx.m[d], smem + (box - smem_base), n_pair + h * 128 + b * 32,
+                              m_cta + q * 32);
         sm100::tma_store_commit();
       }
     }

@@ -168,7 +168,8 @@ template <int V, int R>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(UniCfg::NUM_THREADS, 1)
     tcec_gemm_pair_uni_kernel(const __grid_constant__ CUtensorMap tmA,
                               const __grid_constant__ CUtensorMap tmB,
-                              const __grid_constant__ CUtensorMap tmC, const GemmShape shp,
+                              const __grid_constant__ CUtensorMap tmC,
+                              const __grid_constant__ CDests cx, const GemmShape shp,
                               const float scale, const float inv_scale, const FlagThresholds thr,
                               uint32_t* __restrict__ flags) {
   using C = PairCfg<V>;
@@ -330,6 +331,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(UniCfg::NUM_THREADS,
       __syncwarp();
       if (lane == 0) {
         sm100::tma_store_2d(&tmC, smem + (box - smem_base), n_pair + cb * 64 + b * 32, m_cta + q * 32);
+        for (int d = 0; d < cx.count; ++d)
+          sm100::tma_store_2d(&cx.m[d], smem + (box - smem_base), n_pair + cb * 64 + b * 32,
+                              m_cta + q * 32);
         sm100::tma_store_commit();
       }
     }

@@ -315,6 +315,44 @@ def gemm_device(a, b, scheme="corrected3_halfhalf", cfg: MmaConfig | None = None
     return out
 
 
+def gemm_device_multi(a, b, outs, scheme="corrected3_halfhalf", cfg: MmaConfig | None = None,
+                      flags=None):
+    """C = A @ B stored into every tensor of `outs` (same shape and leading
+    dimension; CUDA memory this GPU can address, e.g. peer buffers of a
+    symmetric-memory all-gather) by one kernel: the fused all-gather path
+    (tcec_sgemm_multi).  Stream-ordered on torch's current stream."""
+    import torch
+
+    variant, rounding, scale = resolve_scheme(scheme)
+    if a.dim() != 2 or b.dim() != 2 or a.shape[1] != b.shape[0]:
+        raise ValueError("gemm expects 2-D matrices with matching inner dimensions")
+    if a.dtype != torch.float32 or b.dtype != torch.float32:
+        raise ValueError("inputs must hold FP32 values")
+    outs = list(outs)
+    if not 1 <= len(outs) <= 8:
+        raise ValueError("1..8 destinations")
+    m, k = a.shape
+    n = b.shape[1]
+    ldc = outs[0].stride(0)
+    for o in outs:
+        if o.shape != (m, n) or o.stride(0) != ldc or o.stride(1) != 1 or o.dtype != torch.float32:
+            raise ValueError("destinations must be float32 (m, n) views with one leading dimension")
+    if ldc % 4:
+        raise ValueError("destination leading dimension must be a multiple of 4")
+    block_k = cfg.block_k if cfg is not None else 16
+    opts = N.make_opts(split_rounding=rounding, scale_log2=scale,
+                       drain_k=drain_k_for(variant, block_k))
+    A, lda = _tma_ready(a)
+    B, ldb = _tma_ready(b)
+    ptrs = (ctypes.c_void_p * len(outs))(*[o.data_ptr() for o in outs])
+    stream = torch.cuda.current_stream(a.device).cuda_stream
+    N.check(N.lib().tcec_sgemm_multi(variant, m, n, k, A.data_ptr(), lda, B.data_ptr(), ldb,
+                                      ptrs, len(outs), ldc, ctypes.byref(opts),
+                                      flags.data_ptr() if flags is not None else None, stream),
+            "tcec_sgemm_multi")
+    return outs[0]
+
+
 def gemm(a, b, scheme, cfg: MmaConfig | None = None, out=None) -> GemmRun:
     """schemes.py:317-373 for the corrected3 schemes, on the GPU.
 

@@ -123,3 +123,47 @@ def _gather_overlapped(a_slab, b, scheme, m_total, world, group, out, compute, c
         out.copy_(result)
         return out
     return result
+
+
+_SYMM_CACHE: dict = {}
+
+
+def sharded_gemm_fused(a_slab, b, scheme="corrected3_halfhalf", *, m_total: int, group=None):
+    """Row-sharded GEMM with the all-gather fused into the GEMM epilogue.
+
+    The full C lives in symmetric memory (torch.distributed._symmetric_memory:
+    one buffer per rank, every peer's buffer mapped into this GPU's address
+    space over NVLink).  One kernel (tcec_sgemm_multi) computes this rank's
+    slab and TMA-stores each output box into the slab's rows of every rank's
+    buffer, so the gather overlaps the GEMM tile by tile with no separate
+    collective; a barrier then makes the peers' stores visible.  Returns this
+    rank's full (m_total x n) C.  Bit-identical to the single-GPU product.
+    """
+    import torch
+    import torch.distributed as dist
+    import torch.distributed._symmetric_memory as symm_mem
+
+    from .schemes import gemm_device_multi
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if world > 8:
+        raise ValueError("the fused all-gather covers at most 8 ranks (one NVLink domain)")
+    per = -(-m_total // world)
+    n = b.shape[1]
+    ldc = max(4, (n + 3) // 4 * 4)
+    grp = group if group is not None else dist.group.WORLD
+    key = (per * world, ldc, str(b.device), id(grp))
+    if key not in _SYMM_CACHE:  # one symmetric buffer per shape, reused across calls
+        full = symm_mem.empty((per * world, ldc), dtype=torch.float32, device=b.device)
+        _SYMM_CACHE[key] = (full, symm_mem.rendezvous(full, grp))
+    full, hdl = _SYMM_CACHE[key]
+    rows = a_slab.shape[0]
+    r0 = rank * per
+    # own buffer first, then the peers'
+    order = [rank] + [r for r in range(world) if r != rank]
+    outs = [hdl.get_buffer(r, (per * world, ldc), torch.float32)[r0:r0 + rows, :n] for r in order]
+    if rows > 0:
+        gemm_device_multi(a_slab, b, outs, scheme)
+    hdl.barrier()
+    return full[:m_total, :n]

@@ -547,3 +547,49 @@ def test_inunit_ragged_vs_oracle(name, shape):
     mag, terms = _inunit_mag(a, b, name)
     bound = (terms * (-(-k // 16)) + 2) * 2.0 ** -22 * mag
     assert np.all(np.abs(run.output.astype(np.float64) - ref) <= bound)
+
+
+@pytest.mark.parametrize("sname,variant,bk,drain", VARIANTS)
+def test_multi_destination_epilogue(sname, variant, bk, drain):
+    """tcec_sgemm_multi (the fused all-gather epilogue): every destination --
+    here separate buffers on this GPU, standing in for peers' symmetric-memory
+    slabs -- receives exactly the single-destination result, at a row offset
+    inside a larger matrix."""
+    import torch
+
+    T = _T()
+    g = torch.Generator(device="cuda")
+    g.manual_seed(7)
+    A = torch.rand((300, 520), generator=g, device="cuda") * 2 - 1
+    B = torch.rand((520, 264), generator=g, device="cuda") * 2 - 1
+    ref = T.gemm_device(A, B, sname)
+    fulls = [torch.full((1000, 268), float("nan"), device="cuda") for _ in range(4)]
+    outs = [f[256:556, :264] for f in fulls]
+    T.gemm_device_multi(A, B, outs, sname)
+    for f in fulls:
+        assert torch.equal(f[256:556, :264], ref)
+        assert torch.isnan(f[:256]).all() and torch.isnan(f[556:]).all()
+
+
+def test_fused_allgather_single_rank():
+    """sharded_gemm_fused on one rank (symmetric-memory path, world size 1)."""
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    T = _T()
+    from paper_2203_03341_b200.sharded import sharded_gemm_fused
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        A = torch.rand((512, 256), device="cuda") * 2 - 1
+        B = torch.rand((256, 384), device="cuda") * 2 - 1
+        C = sharded_gemm_fused(A, B, "corrected3_tf32", m_total=512)
+        torch.cuda.synchronize()
+        assert torch.equal(C, T.gemm_device(A, B, "corrected3_tf32"))
+    finally:
+        dist.destroy_process_group()
