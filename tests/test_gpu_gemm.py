@@ -593,3 +593,32 @@ def test_fused_allgather_single_rank():
         assert torch.equal(C, T.gemm_device(A, B, "corrected3_tf32"))
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("blocks", [(3, 2), (1, 4), (8, 8)])
+@pytest.mark.parametrize("shape", [(1100, 700, 300), (513, 1030, 64), (300, 260, 0)])
+def test_host_path_blockings_bit_identical(shape, blocks):
+    """tcec_sgemm_host streams C in row x column blocks (uploads interleaved,
+    per-block GEMMs on two streams, per-block downloads): every blocking gives
+    the device path's result bit for bit, flags included, ragged edges and
+    k = 0 included."""
+    import ctypes
+
+    import torch
+
+    T = _T()
+    from paper_2203_03341_b200 import _native as N
+
+    m, n, k = shape
+    a = O.urand(m, k, -1, 1, 21)
+    b = O.urand(k, n, -1, 1, 22)
+    ref = T.gemm(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), "corrected3_tf32")
+    c = np.full((m, n), np.nan, dtype=np.float32)
+    opts = N.make_opts(drain_k=0, host_blocks=blocks)
+    fl = ctypes.c_uint32(0)
+    N.check(N.lib().tcec_sgemm_host(N.TCEC_TF32, m, n, k, a.ctypes.data, max(k, 1), b.ctypes.data,
+                                    n, c.ctypes.data, n, ctypes.byref(opts), ctypes.byref(fl),
+                                    None), "host")
+    assert np.array_equal(c, ref.output.cpu().numpy())
+    assert (bool(fl.value & 1), bool(fl.value & 2)) == (ref.flags.saw_overflow,
+                                                        ref.flags.saw_out_of_range)
