@@ -353,8 +353,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PsCfg<V, S>::NUM_THR
         sm100::tmem_ld_32x32b_x16(tmem_P + lane_off + h * NC + c * 16, r);
         sm100::tmem_ld_wait();
 #pragma unroll
-        for (int j = 0; j < 16; ++j)  // schemes.py:300-304: c = RN32(c + partial)
-          acc[c * 16 + j] = __fadd_rn(acc[c * 16 + j], __uint_as_float(r[j]));
+        for (int j = 0; j < 16; j += 2)  // schemes.py:300-304: c = RN32(c + partial), f32x2
+          sm100::fadd2_rn(acc[c * 16 + j], acc[c * 16 + j + 1], __uint_as_float(r[j]),
+                          __uint_as_float(r[j + 1]));
       }
       sm100::tc_fence_before();
       __syncwarp();
