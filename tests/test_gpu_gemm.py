@@ -622,3 +622,40 @@ def test_host_path_blockings_bit_identical(shape, blocks):
     assert np.array_equal(c, ref.output.cpu().numpy())
     assert (bool(fl.value & 1), bool(fl.value & 2)) == (ref.flags.saw_overflow,
                                                         ref.flags.saw_out_of_range)
+
+
+@pytest.mark.parametrize("sname,variant,bk,drain", VARIANTS)
+@pytest.mark.parametrize("shape", [(16384, 16384, 16384), (65536, 1024, 1024), (2048, 2048, 65536)])
+def test_baseline_full_size_configs(sname, variant, bk, drain, shape):
+    """BASELINE.json configs 2 and 4 at their full sizes.  The whole-product oracle
+    is infeasible there, so: (i) a 4 x 32 block from the middle of the product
+    against the oracle with the kernel's drain interval (GEMM tolerance);
+    (ii) separability -- the same rows and columns computed as a small product
+    are bit-identical to the full product's block; (iii) relres vs FP64 on 64
+    rows spread over every tile row, within 2x of cuBLAS SGEMM's."""
+    import torch
+
+    T = _T()
+    m, n, k = shape
+    g = torch.Generator(device="cuda")
+    g.manual_seed(m + n + k)
+    A = torch.rand((m, k), generator=g, device="cuda") * 2 - 1
+    B = torch.rand((k, n), generator=g, device="cuda") * 2 - 1
+    C = T.gemm_device(A, B, sname)
+    r0, c0 = (m // 2) - 2, (n // 2) - 16
+    a = A[r0:r0 + 4].cpu().numpy()
+    b = B[:, c0:c0 + 32].contiguous().cpu().numpy()
+    blk = C[r0:r0 + 4, c0:c0 + 32].cpu().numpy()
+    oc, _ = O.corrected3(a, b, variant, block_k=bk, drain_k=drain)
+    _check_close(blk, oc, a, b, sname, variant)
+    small = T.gemm_device(A[r0:r0 + 4].contiguous(), B[:, c0:c0 + 32].contiguous(), sname)
+    assert np.array_equal(small.cpu().numpy(), blk)
+    rows = torch.arange(3, m, max(1, m // 64), device="cuda")[:64]
+    ref = A[rows].double() @ B.double()
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    S = A[rows] @ B
+    torch.backends.cuda.matmul.allow_tf32 = prev
+    r_tc = float(torch.linalg.norm(ref - C[rows].double()) / torch.linalg.norm(ref))
+    r_sg = float(torch.linalg.norm(ref - S.double()) / torch.linalg.norm(ref))
+    assert r_tc <= 2.0 * r_sg, (r_tc, r_sg)
