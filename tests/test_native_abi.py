@@ -92,3 +92,16 @@ def test_sass_contains_tcgen05_and_tma():
     for mnem in ("UTCHMMA", "LDTM", "UTMALDG", "UTMASTG"):
         assert mnem in out, mnem
     assert re.search(r"\bHMMA\b", out) is None
+
+
+def test_integration_stub_opts_match_header():
+    """The ctypes stub INTEGRATION.md gives a reference maintainer declares the
+    same tcec_opts fields as include/tcec.h (the C side reads the whole struct)."""
+    doc = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    stub = doc.split("class _Opts(ctypes.Structure):")[1].split("]\n")[0]
+    names = re.findall(r'\("(\w+)", ctypes\.c_int32(?: \* (\d+))?\)', stub)
+    hdr = open(HEADER).read()
+    body = re.sub(r"/\*.*?\*/", "", hdr.split("typedef struct tcec_opts {")[1].split("} tcec_opts;")[0],
+                  flags=re.S)
+    fields = re.findall(r"int32_t\s+(\w+)(?:\[(\d+)\])?;", body)
+    assert [(n, c or "1") for n, c in names] == [(n, c or "1") for n, c in fields]
