@@ -457,22 +457,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
       sm100::mbar_wait(p_full, it & 1);
       sm100::tc_fence_after();
 #pragma unroll
-      for (int c = 0; c < ((TCEC_EXP & 2) ? 0 : 8); ++c) {
-        uint32_t r[16];
-        sm100::tmem_ld_32x32b_x16(tmem_P + lane_off + h * 128 + c * 16, r);
+      for (int c = 0; c < ((TCEC_EXP & 2) ? 0 : 16); ++c) {
+        // 8 columns at a time: fewer live temporaries next to the 128 accumulators
+        uint32_t r[8];
+        sm100::tmem_ld_32x32b_x8(tmem_P + lane_off + h * 128 + c * 8, r);
         sm100::tmem_ld_wait();
 #pragma unroll
-        for (int j = 0; j < 16; j += 2) {  // schemes.py:300-304: c = RN32(c + partial)
-          if constexpr (V == kTF32) {
-            // two RN adds per f32x2 instruction (measured +3% for TF32; the FP16
-            // kernel keeps scalar adds: the register pairs make its drain spill)
-            sm100::fadd2_rn(acc[c * 16 + j], acc[c * 16 + j + 1], __uint_as_float(r[j]),
-                            __uint_as_float(r[j + 1]));
-          } else {
-            acc[c * 16 + j] = __fadd_rn(acc[c * 16 + j], __uint_as_float(r[j]));
-            acc[c * 16 + j + 1] = __fadd_rn(acc[c * 16 + j + 1], __uint_as_float(r[j + 1]));
-          }
-        }
+        for (int j = 0; j < 8; j += 2)  // schemes.py:300-304: c = RN32(c + partial), f32x2
+          sm100::fadd2_rn(acc[c * 8 + j], acc[c * 8 + j + 1], __uint_as_float(r[j]),
+                          __uint_as_float(r[j + 1]));
       }
       sm100::tc_fence_before();
       __syncwarp();
