@@ -15,4 +15,9 @@ from .schemes import (SCHEMES_BY_NAME, GemmKind, GemmRun, GemmScheme, MmaConfig,
 from .splitting import (RESIDUAL_SCALE_LOG2, SplitKind, SplitMatrices, SplitScheme,
                         markidis_halfhalf, scaled_halfhalf, split_device, split_matrix, tf32tf32)
 
+try:  # torch.ops.tcec.sgemm (registered when torch is importable)
+    from . import torch_op  # noqa: F401
+except ImportError:  # pragma: no cover
+    torch_op = None
+
 __version__ = "0.1.0"

@@ -659,3 +659,39 @@ def test_baseline_full_size_configs(sname, variant, bk, drain, shape):
     r_tc = float(torch.linalg.norm(ref - C[rows].double()) / torch.linalg.norm(ref))
     r_sg = float(torch.linalg.norm(ref - S.double()) / torch.linalg.norm(ref))
     assert r_tc <= 2.0 * r_sg, (r_tc, r_sg)
+
+
+def test_torch_op_and_cuda_graph():
+    """torch.ops.tcec.sgemm (SURVEY 8(b)'s operator form) equals gemm_device, and
+    the path replays inside a captured CUDA graph (no host synchronisation,
+    tensor maps encoded at capture), bit for bit."""
+    import torch
+
+    T = _T()
+    g = torch.Generator(device="cuda")
+    g.manual_seed(5)
+    A = torch.rand((520, 300), generator=g, device="cuda") * 2 - 1
+    B = torch.rand((300, 260), generator=g, device="cuda") * 2 - 1
+    for variant, sname in ((0, "corrected3_halfhalf"), (1, "corrected3_tf32")):
+        c, fl = torch.ops.tcec.sgemm(A, B, variant, 0)
+        ref = T.gemm_device(A, B, sname)
+        assert torch.equal(c, ref) and int(fl.item()) == 0
+        out = torch.empty_like(ref)
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            T.gemm_device(A, B, sname, out=out)  # warm-up outside capture
+        torch.cuda.current_stream().wait_stream(s)
+        graph = torch.cuda.CUDAGraph()
+        out.zero_()
+        with torch.cuda.graph(graph):
+            T.gemm_device(A, B, sname, out=out)
+        graph.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref)
+        A2 = A.clone()
+        A.mul_(0.5)  # replay sees the new contents of the captured buffers
+        graph.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out, T.gemm_device(A, B, sname))
+        A.copy_(A2)

@@ -105,3 +105,18 @@ def test_integration_stub_opts_match_header():
                   flags=re.S)
     fields = re.findall(r"int32_t\s+(\w+)(?:\[(\d+)\])?;", body)
     assert [(n, c or "1") for n, c in names] == [(n, c or "1") for n, c in fields]
+
+
+def test_torch_op_registered_with_fake_impl():
+    """torch.ops.tcec.sgemm is registered; its fake implementation traces shapes
+    on meta tensors (no GPU needed), and CPU tensors are refused."""
+    import torch
+
+    import paper_2203_03341_b200  # noqa: F401  (registers the op)
+
+    a = torch.empty((64, 32), device="meta")
+    b = torch.empty((32, 48), device="meta")
+    c, fl = torch.ops.tcec.sgemm(a, b, 1, 0)
+    assert c.shape == (64, 48) and fl.dtype == torch.int32
+    with pytest.raises(Exception):
+        torch.ops.tcec.sgemm(torch.zeros(4, 4), torch.zeros(4, 4), 1, 0)
