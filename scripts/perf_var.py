@@ -12,7 +12,7 @@ rows = torch.arange(0, n, 128, device="cuda")
 torch.backends.cuda.matmul.allow_tf32 = False
 ref = A[rows].double() @ B.double()
 e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
-for kv in [int(x) for x in os.environ.get("KVS", "0,2").split(",")]:
+for kv in [int(x) for x in os.environ.get("KVS", "0,1").split(",")]:
     for pf in [int(x) for x in os.environ.get("PFS", "0").split(",")]:
         out = {"kernel_variant": kv, "prefetch": pf}
         for v in ("corrected3_halfhalf", "corrected3_tf32"):
