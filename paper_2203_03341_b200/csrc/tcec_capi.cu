@@ -18,6 +18,7 @@
 #include "tcec_gemm2.cuh"
 #include "tcec_gemm3.cuh"
 #include "tcec_gemm4.cuh"
+#include "tcec_gemm5.cuh"
 #include "tcec_presplit.cuh"
 #include "tcec_census.cuh"
 
@@ -307,6 +308,52 @@ int launch_gemm_presplit(int64_t m, int64_t n, int64_t k, const float* A, int64_
   return st;
 }
 
+// Persistent CTA-pair kernel (kernel_variant 2): one pair per TPC walks the
+// tile sequence with its pipelines running across tiles.
+template <int V, int R>
+int launch_gemm_pers(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, const float* B,
+                     int64_t ldb, float* C, int64_t ldc, int scale_log2, int drain_every,
+                     int group_m, uint32_t* d_flags, cudaStream_t stream) {
+  using Cfg = tcec::PairCfg<V>;
+  using VC = tcec::VarCfg<V>;
+  CUtensorMap tmA, tmB;
+  int st;
+  if ((st = make_tmap(&tmA, A, k, m, lda, Cfg::BK_STG, Cfg::BM, CU_TENSOR_MAP_SWIZZLE_128B)))
+    return st;
+  if ((st = make_tmap(&tmB, B, n, k, ldb, 32, Cfg::BK_STG, CU_TENSOR_MAP_SWIZZLE_128B))) return st;
+  auto kern = tcec::tcec_gemm_pers_kernel<V, R>;
+  static std::once_flag attr_once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(attr_once, [&] {
+    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    Cfg::SMEM_BYTES);
+  });
+  if (attr_err != cudaSuccess) return TCEC_ERR_CUDA;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  tcec::GemmShape shp;
+  shp.m = static_cast<int32_t>(m);
+  shp.n = static_cast<int32_t>(n);
+  shp.k = static_cast<int32_t>(k);
+  shp.num_op_stages = static_cast<int32_t>((k + VC::BK_OP - 1) / VC::BK_OP);
+  shp.drain_every = drain_every;
+  shp.group_m = group_m;
+  shp.prefetch = 0;
+  shp.mma_order = 0;
+  const float scale = ldexpf(1.0f, scale_log2);
+  const float inv_scale = ldexpf(1.0f, -scale_log2);
+  const tcec::FlagThresholds thr = tcec::flag_thresholds(V, R, scale_log2);
+  const int64_t tiles = ((m + 2 * Cfg::BM - 1) / (2 * Cfg::BM)) * ((n + Cfg::BN - 1) / Cfg::BN);
+  int64_t pairs = sms / 2;
+  if (pairs > tiles) pairs = tiles;
+  if (pairs < 1) pairs = 1;
+  kern<<<static_cast<unsigned>(2 * pairs), Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream>>>(
+      tmA, tmB, C, ldc, shp, scale, inv_scale, thr, d_flags);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError() == cudaSuccess ? TCEC_OK : TCEC_ERR_CUDA;
+}
+
 template <int V, int R>
 int dispatch_bn(int bn, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda,
                 const float* B, int64_t ldb, float* C, int64_t ldc, int s, int de, int gm, int pf,
@@ -332,6 +379,11 @@ int dispatch_bn(int bn, int64_t m, int64_t n, int64_t k, const float* A, int64_t
   }
   switch (bn) {
     case 256:
+      if (kv == 2) {
+        if (ex && ex->count > 0) return TCEC_ERR_UNSUPPORTED;
+        return launch_gemm_pers<V, R>(m, n, k, A, lda, B, ldb, C, ldc, s, de,
+                                      gm / 2 > 0 ? gm / 2 : 1, fl, st);
+      }
       if (kv == 1)
         return launch_gemm_pair<V, R, true>(m, n, k, A, lda, B, ldb, C, ldc, s, de,
                                             gm / 2 > 0 ? gm / 2 : 1, pf, mo, ex, fl, st);
