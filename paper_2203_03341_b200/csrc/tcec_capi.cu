@@ -313,7 +313,7 @@ int launch_gemm_presplit(int64_t m, int64_t n, int64_t k, const float* A, int64_
 template <int V, int R>
 int launch_gemm_pers(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, const float* B,
                      int64_t ldb, float* C, int64_t ldc, int scale_log2, int drain_every,
-                     int group_m, uint32_t* d_flags, cudaStream_t stream) {
+                     int group_m, bool lockstep, uint32_t* d_flags, cudaStream_t stream) {
   using Cfg = tcec::PairCfg<V>;
   using VC = tcec::VarCfg<V>;
   CUtensorMap tmA, tmB;
@@ -348,8 +348,19 @@ int launch_gemm_pers(int64_t m, int64_t n, int64_t k, const float* A, int64_t ld
   int64_t pairs = sms / 2;
   if (pairs > tiles) pairs = tiles;
   if (pairs < 1) pairs = 1;
+  uint32_t* wave_ctr = nullptr;
+  if (lockstep) {  // one counter per device, zeroed in stream order before each launch
+    static uint32_t* ctr[64] = {};
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
+    if (dev < 0 || dev >= 64) return TCEC_ERR_CUDA;
+    if (!ctr[dev] && cudaMalloc(reinterpret_cast<void**>(&ctr[dev]), sizeof(uint32_t)) != cudaSuccess)
+      return TCEC_ERR_CUDA;
+    wave_ctr = ctr[dev];
+    if (cudaMemsetAsync(wave_ctr, 0, sizeof(uint32_t), stream) != cudaSuccess) return TCEC_ERR_CUDA;
+  }
   kern<<<static_cast<unsigned>(2 * pairs), Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream>>>(
-      tmA, tmB, C, ldc, shp, scale, inv_scale, thr, d_flags);
+      tmA, tmB, C, ldc, shp, scale, inv_scale, thr, d_flags, wave_ctr);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError() == cudaSuccess ? TCEC_OK : TCEC_ERR_CUDA;
 }
@@ -358,7 +369,7 @@ template <int V, int R>
 int dispatch_bn(int bn, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda,
                 const float* B, int64_t ldb, float* C, int64_t ldc, int s, int de, int gm, int pf,
                 int kv, int mo, int sm, int sch, const ExtraC* ex, uint32_t* fl,
-                cudaStream_t st) {
+                cudaStream_t st, int gm_user) {
   if (ex && ex->count > 0 && (bn != 256 || sm == 2 || sch != TCEC_SCHEME_CORRECTED3))
     return TCEC_ERR_UNSUPPORTED;  // extra destinations: the default pair kernels only
   if (sm == 2 || sch != TCEC_SCHEME_CORRECTED3) {
@@ -378,18 +389,33 @@ int dispatch_bn(int bn, int64_t m, int64_t n, int64_t k, const float* A, int64_t
     }
   }
   switch (bn) {
-    case 256:
-      if (kv == 2) {
-        if (ex && ex->count > 0) return TCEC_ERR_UNSUPPORTED;
-        return launch_gemm_pers<V, R>(m, n, k, A, lda, B, ldb, C, ldc, s, de,
-                                      gm / 2 > 0 ? gm / 2 : 1, fl, st);
+    case 256: {
+      // kernel_variant 0 = automatic: the persistent kernel with lock-step waves
+      // of 8 x 9 pair tiles once the product spans >= 16 waves (measured +2-8% at
+      // 16384^3 and 32768 x 16384^2, DRAM reads -21%), else the per-tile kernel
+      const int64_t tiles = ((m + 255) / 256) * ((n + 255) / 256);
+      int sms = 148;
+      {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       }
+      if (kv == 0)
+        kv = (tiles >= 16 * int64_t(sms / 2) && !(ex && ex->count > 0) && mo == 0 && pf == 0) ? 3
+                                                                                         : 4;
+      if (kv == 2 || kv == 3) {  // persistent; 3 = with lock-step waves
+        if (ex && ex->count > 0) return TCEC_ERR_UNSUPPORTED;
+        const int g = gm_user > 0 ? (gm / 2 > 0 ? gm / 2 : 1) : (kv == 3 ? 8 : 4);
+        return launch_gemm_pers<V, R>(m, n, k, A, lda, B, ldb, C, ldc, s, de, g, kv == 3, fl, st);
+      }
+      if (kv == 4) kv = 0;  // the per-tile pair kernel
       if (kv == 1)
         return launch_gemm_pair<V, R, true>(m, n, k, A, lda, B, ldb, C, ldc, s, de,
                                             gm / 2 > 0 ? gm / 2 : 1, pf, mo, ex, fl, st);
       if (kv != 0) return TCEC_ERR_UNSUPPORTED;
       return launch_gemm_pair<V, R, false>(m, n, k, A, lda, B, ldb, C, ldc, s, de,
                                            gm / 2 > 0 ? gm / 2 : 1, pf, mo, ex, fl, st);
+    }
     case 192:
       if (kv != 0) return TCEC_ERR_UNSUPPORTED;
       return launch_gemm_ts<V, R, 192, 2>(m, n, k, A, lda, B, ldb, C, ldc, s, de,
@@ -487,8 +513,10 @@ int sgemm_impl(int variant, int64_t m, int64_t n, int64_t k, const float* A, int
   const int group_m = o.group_m <= 0 ? 8 : o.group_m;
   // reserved[0]: L2 prefetch distance in 32-deep k-slices (pair kernel; 0 = off)
   const int prefetch = o.reserved[0] < 0 ? 0 : (o.reserved[0] > 16 ? 16 : o.reserved[0]);
-  // reserved[1]: pair-kernel variant (0 = split + drain warps, 1 = unified split/drain workers)
+  // reserved[1]: pair-kernel variant (0 = automatic, 1 = unified split/drain workers,
+  // 2 = persistent, 3 = persistent with lock-step waves, 4 = per-tile)
   const int kvariant = o.reserved[1];
+  if (kvariant < 0 || kvariant > 4) return TCEC_ERR_UNSUPPORTED;
   // reserved[2]: pair-kernel MMA order (0 = corrections then main term, 1 = A_hi collector reuse)
   const int mma_order = o.reserved[2];
   if (mma_order != 0 && mma_order != 1) return TCEC_ERR_UNSUPPORTED;
@@ -515,21 +543,21 @@ int sgemm_impl(int variant, int64_t m, int64_t n, int64_t k, const float* A, int
   if (variant == TCEC_FP16) {
     if (rounding == TCEC_ROUND_RN)
       return dispatch_bn<tcec::kFP16, tcec::kRN>(block_n, m, n, k, A, lda, B, ldb, C, ldc,
-                                                 scale_log2, drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, ex, d_flags, st);
+                                                 scale_log2, drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, ex, d_flags, st, o.group_m);
     if (rounding == TCEC_ROUND_RZ)
       return dispatch_bn<tcec::kFP16, tcec::kRZ>(block_n, m, n, k, A, lda, B, ldb, C, ldc,
-                                                 scale_log2, drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, ex, d_flags, st);
+                                                 scale_log2, drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, ex, d_flags, st, o.group_m);
     return TCEC_ERR_UNSUPPORTED;
   }
   if (rounding == TCEC_ROUND_RNA)
     return dispatch_bn<tcec::kTF32, tcec::kRNA>(block_n, m, n, k, A, lda, B, ldb, C, ldc, 0,
-                                                drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, ex, d_flags, st);
+                                                drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, ex, d_flags, st, o.group_m);
   if (rounding == TCEC_ROUND_RN)
     return dispatch_bn<tcec::kTF32, tcec::kRN>(block_n, m, n, k, A, lda, B, ldb, C, ldc, 0,
-                                               drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, ex, d_flags, st);
+                                               drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, ex, d_flags, st, o.group_m);
   if (rounding == TCEC_ROUND_RZ)
     return dispatch_bn<tcec::kTF32, tcec::kRZ>(block_n, m, n, k, A, lda, B, ldb, C, ldc, 0,
-                                               drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, ex, d_flags, st);
+                                               drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, ex, d_flags, st, o.group_m);
   return TCEC_ERR_UNSUPPORTED;
 }
 

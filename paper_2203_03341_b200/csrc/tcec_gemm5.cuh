@@ -70,7 +70,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
                           const __grid_constant__ CUtensorMap tmB,  // B [k][n], box 32 x 32, SW128
                           float* __restrict__ Cout, const int64_t ldc, const GemmShape shp,
                           const float scale, const float inv_scale, const FlagThresholds thr,
-                          uint32_t* __restrict__ flags) {
+                          uint32_t* __restrict__ flags, uint32_t* __restrict__ wave_ctr) {
   using C = PairCfg<V>;
   using VC = VarCfg<V>;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -130,7 +130,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
     if (warp == 0 && lane == 0) {
       // ===================== TMA producer =====================
       uint32_t gst = 0;
-      for (int tile = pid; tile < num_tiles; tile += npairs) {
+      uint32_t target = 0;
+      int wave = 0;
+      for (int tile = pid; tile < num_tiles; tile += npairs, ++wave) {
+        if (wave_ctr != nullptr && wave > 0) {
+          // lock-step waves: the CTAs that have a tile in this wave all finish
+          // issuing the previous wave's loads before any starts this one, so the
+          // tiles of a wave read the same k-slices while they are in L2.
+          // Arrivals for wave w come from the 2 min(P, T - wP) CTAs with a wave-w tile.
+          target += 2u * static_cast<uint32_t>(min(npairs, num_tiles - wave * npairs));
+          // The wait is bounded (~0.2 ms): the barrier only shapes L2 reuse, so a
+          // CTA that cannot see its peers (e.g. not co-resident because another
+          // kernel holds SMs) goes on instead of deadlocking.
+          atomicAdd(wave_ctr, 1u);
+          uint32_t v;
+          for (int spin = 0; spin < 2000; ++spin) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(wave_ctr) : "memory");
+            if (v >= target) break;
+            __nanosleep(100);
+          }
+        }
         int tm, tn;
         grouped_tile(tile, tiles_m, tiles_n, shp.group_m, tm, tn);
         const int m_cta = tm * 2 * C::BM + rank * C::BM;
