@@ -87,7 +87,7 @@ typedef struct tcec_opts {
   int32_t host_col_blocks;
   /* reserved[0]: L2 prefetch distance in 32-deep k-slices (0 = off);
    * reserved[1]: pair-kernel variant (0 = automatic: persistent with lock-step waves for
-   *              products of >= 16 waves of tiles, else per-tile; 1 = unified split/drain
+   *              products of >= 8 waves of tiles, else per-tile; 1 = unified split/drain
    *              workers; 2 = persistent; 3 = persistent, lock-step waves; 4 = per-tile);
    * reserved[2]: pair-kernel MMA order (0 = corrections first, 1 = A_hi collector reuse). */
   int32_t reserved[3];

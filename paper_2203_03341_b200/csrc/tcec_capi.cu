@@ -391,8 +391,8 @@ int dispatch_bn(int bn, int64_t m, int64_t n, int64_t k, const float* A, int64_t
   switch (bn) {
     case 256: {
       // kernel_variant 0 = automatic: the persistent kernel with lock-step waves
-      // of 8 x 9 pair tiles once the product spans >= 16 waves (measured +2-8% at
-      // 16384^3 and 32768 x 16384^2, DRAM reads -21%), else the per-tile kernel
+      // of 8 x 9 pair tiles once the product spans >= 8 waves (measured +2-8% at
+      // 8192^3 .. 32768 x 16384^2, DRAM reads -21..-52%), else the per-tile kernel
       const int64_t tiles = ((m + 255) / 256) * ((n + 255) / 256);
       int sms = 148;
       {
@@ -401,7 +401,7 @@ int dispatch_bn(int bn, int64_t m, int64_t n, int64_t k, const float* A, int64_t
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       }
       if (kv == 0)
-        kv = (tiles >= 16 * int64_t(sms / 2) && !(ex && ex->count > 0) && mo == 0 && pf == 0) ? 3
+        kv = (tiles >= 8 * int64_t(sms / 2) && !(ex && ex->count > 0) && mo == 0 && pf == 0) ? 3
                                                                                          : 4;
       if (kv == 2 || kv == 3) {  // persistent; 3 = with lock-step waves
         if (ex && ex->count > 0) return TCEC_ERR_UNSUPPORTED;
