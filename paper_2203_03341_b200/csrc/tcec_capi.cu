@@ -373,7 +373,7 @@ int dispatch_bn(int bn, int64_t m, int64_t n, int64_t k, const float* A, int64_t
   if (ex && ex->count > 0 && (bn != 256 || sm == 2 || sch != TCEC_SCHEME_CORRECTED3))
     return TCEC_ERR_UNSUPPORTED;  // extra destinations: the default pair kernels only
   if (sm == 2 || sch != TCEC_SCHEME_CORRECTED3) {
-    if ((bn != 256 && bn != 0) || kv != 0 || mo != 0) return TCEC_ERR_UNSUPPORTED;
+    if ((bn != 256 && bn != 0) || (kv != 0 && kv != 4) || mo != 0) return TCEC_ERR_UNSUPPORTED;
     const int g = gm / 2 > 0 ? gm / 2 : 1;
     switch (sch) {
       case TCEC_SCHEME_CORRECTED3:
@@ -417,7 +417,7 @@ int dispatch_bn(int bn, int64_t m, int64_t n, int64_t k, const float* A, int64_t
                                            gm / 2 > 0 ? gm / 2 : 1, pf, mo, ex, fl, st);
     }
     case 192:
-      if (kv != 0) return TCEC_ERR_UNSUPPORTED;
+      if (kv != 0 && kv != 4) return TCEC_ERR_UNSUPPORTED;
       return launch_gemm_ts<V, R, 192, 2>(m, n, k, A, lda, B, ldb, C, ldc, s, de,
                                            gm / 2 > 0 ? gm / 2 : 1, fl, st);
     case 128:
@@ -627,6 +627,14 @@ int tcec_sgemm_host(int variant, int64_t m, int64_t n, int64_t k, const float* A
     int64_t sz = ((extent + nb - 1) / nb + 255) / 256 * 256;
     return sz < 256 ? int64_t(256) : sz;
   };
+  // The blocks run on two concurrent streams: keep them on the per-tile kernel
+  // (the persistent lock-step kernel assumes it has the GPU to itself).
+  tcec_opts bo;
+  memset(&bo, 0, sizeof(bo));
+  bo.split_rounding = TCEC_ROUND_DEFAULT;
+  bo.scale_log2 = -1;
+  if (opts) bo = *opts;
+  if (bo.reserved[1] == 0) bo.reserved[1] = 4;
   const int64_t rb = blocks(m, opts ? opts->host_row_blocks : 0, 8);
   const int64_t cbk = blocks(n, opts ? opts->host_col_blocks : 0, variant == TCEC_FP16 ? 4 : 8);
   const int R = static_cast<int>((m + rb - 1) / rb);
@@ -688,7 +696,7 @@ int tcec_sgemm_host(int variant, int64_t m, int64_t n, int64_t k, const float* A
         ok = cu(cudaStreamWaitEvent(sc, ev_a[i], 0)) && cu(cudaStreamWaitEvent(sc, ev_b[j], 0));
         if (!ok) break;
         const int s2 = tcec_sgemm(variant, rows, cols, k, dA + r0 * dlda, dlda, dB + c0, dldb,
-                                  dC + r0 * dldc + c0, dldc, opts, dF, sc);
+                                  dC + r0 * dldc + c0, dldc, &bo, dF, sc);
         if (s2 != TCEC_OK) {
           status = s2;
           ok = false;
