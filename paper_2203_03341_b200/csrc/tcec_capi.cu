@@ -349,20 +349,21 @@ int launch_gemm_pers(int64_t m, int64_t n, int64_t k, const float* A, int64_t ld
   if (pairs > tiles) pairs = tiles;
   if (pairs < 1) pairs = 1;
   uint32_t* wave_ctr = nullptr;
-  if (lockstep) {  // one counter per device, zeroed in stream order before each launch
-    static uint32_t* ctr[64] = {};
-    static std::mutex mu;
-    std::lock_guard<std::mutex> lk(mu);
-    if (dev < 0 || dev >= 64) return TCEC_ERR_CUDA;
-    if (!ctr[dev] && cudaMalloc(reinterpret_cast<void**>(&ctr[dev]), sizeof(uint32_t)) != cudaSuccess)
+  if (lockstep) {  // a zeroed counter per launch, from the stream-ordered pool
+    keep_pool(dev);
+    if (cudaMallocAsync(reinterpret_cast<void**>(&wave_ctr), sizeof(uint32_t), stream) != cudaSuccess)
       return TCEC_ERR_CUDA;
-    wave_ctr = ctr[dev];
-    if (cudaMemsetAsync(wave_ctr, 0, sizeof(uint32_t), stream) != cudaSuccess) return TCEC_ERR_CUDA;
+    if (cudaMemsetAsync(wave_ctr, 0, sizeof(uint32_t), stream) != cudaSuccess) {
+      cudaFreeAsync(wave_ctr, stream);
+      return TCEC_ERR_CUDA;
+    }
   }
   kern<<<static_cast<unsigned>(2 * pairs), Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream>>>(
       tmA, tmB, C, ldc, shp, scale, inv_scale, thr, d_flags, wave_ctr);
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  return cudaGetLastError() == cudaSuccess ? TCEC_OK : TCEC_ERR_CUDA;
+  const bool launched = cudaGetLastError() == cudaSuccess;
+  if (wave_ctr) cudaFreeAsync(wave_ctr, stream);
+  return launched ? TCEC_OK : TCEC_ERR_CUDA;
 }
 
 template <int V, int R>

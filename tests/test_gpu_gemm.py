@@ -696,3 +696,40 @@ def test_torch_op_and_cuda_graph():
         torch.cuda.synchronize()
         assert torch.equal(out, T.gemm_device(A, B, sname))
         A.copy_(A2)
+
+
+def test_lockstep_kernel_in_cuda_graph_and_concurrent_streams():
+    """The persistent lock-step kernel (kernel_variant=3; a per-launch wave counter
+    from the stream-ordered pool) captures into a CUDA graph, and two launches
+    running concurrently on two streams -- which cannot all be co-resident, so
+    the bounded wave barrier must give way -- still finish with exact results."""
+    import torch
+
+    T = _T()
+    g = torch.Generator(device="cuda")
+    g.manual_seed(9)
+    A = torch.rand((2048, 512), generator=g, device="cuda") * 2 - 1
+    B = torch.rand((512, 4096), generator=g, device="cuda") * 2 - 1
+    ref = T.gemm_device(A, B, "corrected3_tf32", kernel_variant=4)
+    out = torch.empty_like(ref)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        T.gemm_device(A, B, "corrected3_tf32", out=out, kernel_variant=3)
+    torch.cuda.current_stream().wait_stream(s)
+    graph = torch.cuda.CUDAGraph()
+    out.zero_()
+    with torch.cuda.graph(graph):
+        T.gemm_device(A, B, "corrected3_tf32", out=out, kernel_variant=3)
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
+    outs = [torch.empty_like(ref) for _ in range(2)]
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    for st, o in zip(streams, outs):
+        st.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(st):
+            T.gemm_device(A, B, "corrected3_tf32", out=o, kernel_variant=3)
+    torch.cuda.synchronize()
+    for o in outs:
+        assert torch.equal(o, ref)
