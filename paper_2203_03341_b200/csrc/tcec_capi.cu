@@ -242,7 +242,8 @@ int launch_gemm_ts(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda,
 template <int V, int R, int S>
 int launch_gemm_presplit(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda,
                          const float* B, int64_t ldb, float* C, int64_t ldc, int scale_log2,
-                         int drain_every, int group_m, uint32_t* d_flags, cudaStream_t stream) {
+                         int drain_every, int group_m, int group_user, bool lockstep_ok,
+                         uint32_t* d_flags, cudaStream_t stream) {
   using Cfg = tcec::PsCfg<V, S>;
   using VC = tcec::VarCfg<V>;
   const uint32_t esize = V == tcec::kFP16 ? 2u : 4u;
@@ -261,12 +262,11 @@ int launch_gemm_presplit(int64_t m, int64_t n, int64_t k, const float* A, int64_
   void* bh = ws + 2 * a_bytes;
   void* bl = ws + 2 * a_bytes + b_bytes;
   int st = TCEC_OK;
-  CUtensorMap tmAh, tmAl, tmBh, tmBl, tmC;
+  CUtensorMap tmAh, tmAl, tmBh, tmBl;
   if (!st) st = make_tmap_op(&tmAh, ah, dt, esize, k, m, ldk, Cfg::BM);
   if (!st) st = make_tmap_op(&tmAl, al, dt, esize, k, m, ldk, Cfg::BM);
   if (!st) st = make_tmap_op(&tmBh, bh, dt, esize, k, n, ldk, Cfg::BN_CTA);
   if (!st) st = make_tmap_op(&tmBl, bl, dt, esize, k, n, ldk, Cfg::BN_CTA);
-  if (!st) st = make_tmap(&tmC, C, n, m, ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
   auto kern = tcec::tcec_gemm_ps_kernel<V, S>;
   static std::once_flag attr_once;
   static cudaError_t attr_err = cudaSuccess;
@@ -275,6 +275,20 @@ int launch_gemm_presplit(int64_t m, int64_t n, int64_t k, const float* A, int64_
                                     Cfg::SMEM_BYTES);
   });
   if (!st && attr_err != cudaSuccess) st = TCEC_ERR_CUDA;
+  // persistent: one pair per TPC; lock-step waves of 8 x 9 tiles from 8 waves on
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t tiles = ((m + 2 * Cfg::BM - 1) / (2 * Cfg::BM)) * ((n + Cfg::BN - 1) / Cfg::BN);
+  int64_t pairs = sms / 2;
+  if (pairs > tiles) pairs = tiles;
+  if (pairs < 1) pairs = 1;
+  const bool lockstep = lockstep_ok && tiles >= 8 * int64_t(sms / 2);
+  uint32_t* wave_ctr = nullptr;
+  if (!st && lockstep) {
+    if (cudaMallocAsync(reinterpret_cast<void**>(&wave_ctr), sizeof(uint32_t), stream) != cudaSuccess ||
+        cudaMemsetAsync(wave_ctr, 0, sizeof(uint32_t), stream) != cudaSuccess)
+      st = TCEC_ERR_CUDA;
+  }
   if (!st) {
     const float scale = ldexpf(1.0f, scale_log2);
     const float inv_scale = ldexpf(1.0f, -scale_log2);
@@ -295,15 +309,15 @@ int launch_gemm_presplit(int64_t m, int64_t n, int64_t k, const float* A, int64_
     shp.k = static_cast<int32_t>(k);
     shp.num_op_stages = static_cast<int32_t>((k + VC::BK_OP - 1) / VC::BK_OP);
     shp.drain_every = drain_every;
-    shp.group_m = group_m;
+    shp.group_m = group_user > 0 ? group_m : (lockstep ? 8 : group_m);
     shp.prefetch = 0;
     shp.mma_order = 0;
-    const int64_t pairs = ((m + 2 * Cfg::BM - 1) / (2 * Cfg::BM)) * ((n + Cfg::BN - 1) / Cfg::BN);
     kern<<<static_cast<unsigned>(2 * pairs), Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream>>>(
-        tmAh, tmAl, tmBh, tmBl, tmC, shp, inv_scale, inv_scale2, d_flags);
+        tmAh, tmAl, tmBh, tmBl, C, ldc, shp, inv_scale, inv_scale2, d_flags, wave_ctr);
     g_launches.fetch_add(3, std::memory_order_relaxed);
     if (cudaGetLastError() != cudaSuccess) st = TCEC_ERR_CUDA;
   }
+  if (wave_ctr) cudaFreeAsync(wave_ctr, stream);
   cudaFreeAsync(ws, stream);
   return st;
 }
@@ -376,15 +390,16 @@ int dispatch_bn(int bn, int64_t m, int64_t n, int64_t k, const float* A, int64_t
   if (sm == 2 || sch != TCEC_SCHEME_CORRECTED3) {
     if ((bn != 256 && bn != 0) || (kv != 0 && kv != 4) || mo != 0) return TCEC_ERR_UNSUPPORTED;
     const int g = gm / 2 > 0 ? gm / 2 : 1;
+    const bool ls = kv != 4;  // the host path's concurrent blocks pin variant 4
     switch (sch) {
       case TCEC_SCHEME_CORRECTED3:
-        return launch_gemm_presplit<V, R, tcec::kSchC3>(m, n, k, A, lda, B, ldb, C, ldc, s, de, g, fl, st);
+        return launch_gemm_presplit<V, R, tcec::kSchC3>(m, n, k, A, lda, B, ldb, C, ldc, s, de, g, gm_user, ls, fl, st);
       case TCEC_SCHEME_CORRECTED3_DD:
-        return launch_gemm_presplit<V, R, tcec::kSchC3DD>(m, n, k, A, lda, B, ldb, C, ldc, s, de, g, fl, st);
+        return launch_gemm_presplit<V, R, tcec::kSchC3DD>(m, n, k, A, lda, B, ldb, C, ldc, s, de, g, gm_user, ls, fl, st);
       case TCEC_SCHEME_TC_PLAIN:
-        return launch_gemm_presplit<V, R, tcec::kSchPlain>(m, n, k, A, lda, B, ldb, C, ldc, 0, de, g, fl, st);
+        return launch_gemm_presplit<V, R, tcec::kSchPlain>(m, n, k, A, lda, B, ldb, C, ldc, 0, de, g, gm_user, ls, fl, st);
       case TCEC_SCHEME_INUNIT4:
-        return launch_gemm_presplit<V, R, tcec::kSchIn4>(m, n, k, A, lda, B, ldb, C, ldc, s, de, g, fl, st);
+        return launch_gemm_presplit<V, R, tcec::kSchIn4>(m, n, k, A, lda, B, ldb, C, ldc, s, de, g, gm_user, ls, fl, st);
       default:
         return TCEC_ERR_UNSUPPORTED;
     }

@@ -20,7 +20,7 @@
 // where hi overflowed.
 #pragma once
 
-#include "tcec_gemm2.cuh"
+#include "tcec_gemm5.cuh"
 
 namespace tcec {
 
@@ -199,9 +199,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PsCfg<V, S>::NUM_THR
                         const __grid_constant__ CUtensorMap tmAl,  // A_lo
                         const __grid_constant__ CUtensorMap tmBh,  // B_hi^T [n][k] box 128B x 128
                         const __grid_constant__ CUtensorMap tmBl,  // B_lo^T
-                        const __grid_constant__ CUtensorMap tmC,   // C [m][n], box 32 x 32, SW128
-                        const GemmShape shp, const float inv_scale, const float inv_scale2,
-                        uint32_t* __restrict__ flags) {
+                        float* __restrict__ Cout, const int64_t ldc, const GemmShape shp,
+                        const float inv_scale, const float inv_scale2, uint32_t* __restrict__ flags,
+                        uint32_t* __restrict__ wave_ctr) {
+  // Persistent: one CTA pair per TPC walks the tile sequence (grouped raster),
+  // ring / drain counters running across tiles; `acc_empty` orders each tile's
+  // epilogue reads of the accumulators before the next tile's first MMA into
+  // them; with `wave_ctr` the TMA producers meet once per wave (bounded wait)
+  // so each wave's tiles share L2-resident k-slices (as tcec_gemm5.cuh).
   using C = PsCfg<V, S>;
   using VC = VarCfg<V>;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -210,32 +215,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PsCfg<V, S>::NUM_THR
   uint64_t* op_empty = bars + C::NOP;       // MMA commit -> TMA        (both, multicast)
   uint64_t* p_full = bars + 2 * C::NOP;     // MMA commit -> drain      (both, multicast)
   uint64_t* p_empty = p_full + 1;           // drain -> MMA             (leader, 16)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NUM_BARS);
+  uint64_t* acc_empty = bars + C::NUM_BARS; // epilogue -> next tile's MMA (leader, 16)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NUM_BARS + 1);
   const uint32_t smem_base = sm100::smem_u32(smem);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t rank = sm100::cluster_ctarank();
-
   const int tiles_m = (shp.m + 2 * C::BM - 1) / (2 * C::BM);
   const int tiles_n = (shp.n + C::BN - 1) / C::BN;
-  int tile_m, tile_n;
-  {
-    const int pid = blockIdx.x >> 1;
-    const int per_group = shp.group_m * tiles_n;
-    const int g = pid / per_group;
-    const int first_m = g * shp.group_m;
-    const int gsize = min(tiles_m - first_m, shp.group_m);
-    const int in_g = pid - g * per_group;
-    tile_m = first_m + in_g % gsize;
-    tile_n = in_g / gsize;
-  }
-  const int m_cta = tile_m * 2 * C::BM + rank * C::BM;
-  const int n_pair = tile_n * C::BN;
-  const int n_cta = n_pair + rank * C::BN_CTA;
+  const int num_tiles = tiles_m * tiles_n;
+  const int npairs = gridDim.x >> 1;
+  const int pid = blockIdx.x >> 1;
   const int nop = shp.num_op_stages;
   const int de = shp.drain_every;
-  const int nintervals = C::kDrain ? (nop + de - 1) / de : 0;
+  const int nintervals = C::kDrain ? (nop + de - 1) / de : 1;
 
   if (warp == 0 && lane == 0) {
     if (smem_base & 1023u) __trap();
@@ -243,13 +237,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PsCfg<V, S>::NUM_THR
     sm100::tma_prefetch_desc(&tmAl);
     sm100::tma_prefetch_desc(&tmBh);
     sm100::tma_prefetch_desc(&tmBl);
-    sm100::tma_prefetch_desc(&tmC);
     for (int o = 0; o < C::NOP; ++o) {
       sm100::mbar_init(&op_full[o], 1);
       sm100::mbar_init(&op_empty[o], 1);
     }
     sm100::mbar_init(p_full, 1);
     sm100::mbar_init(p_empty, 2 * C::NUM_DRAIN_WARPS);
+    sm100::mbar_init(acc_empty, 2 * C::NUM_DRAIN_WARPS);
     sm100::fence_mbar_init();
   }
   if (warp == 2) sm100::tmem_alloc_pair<C::TMEM_COLS>(tmem_slot);
@@ -265,73 +259,100 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PsCfg<V, S>::NUM_THR
     if (warp == 0 && lane == 0) {
       // ===================== TMA producer (both CTAs) =====================
       const uint32_t leader_full = sm100::mapa_shared(sm100::smem_u32(op_full), 0);
-      for (int kb = 0; kb < nop; ++kb) {
-        const int o = kb % C::NOP;
-        sm100::mbar_wait(&op_empty[o], ((kb / C::NOP) & 1) ^ 1);
-        if (rank == 0) sm100::mbar_arrive_expect_tx(&op_full[o], 2 * C::OP_BYTES);
-        const uint32_t dst = smem_base + C::OFF_OP + o * C::OP_BYTES;
-        const uint32_t bar = leader_full + o * 8;
-        const int kc = kb * VC::BK_OP;
-        tma_load_2d_pair(dst + C::OFF_AHI, &tmAh, bar, kc, m_cta);
-        tma_load_2d_pair(dst + C::OFF_BHI, &tmBh, bar, kc, n_cta);
-        if constexpr (C::kLo) {
-          tma_load_2d_pair(dst + C::OFF_ALO, &tmAl, bar, kc, m_cta);
-          tma_load_2d_pair(dst + C::OFF_BLO, &tmBl, bar, kc, n_cta);
+      uint32_t g = 0, target = 0;
+      int wave = 0;
+      for (int tile = pid; tile < num_tiles; tile += npairs, ++wave) {
+        if (wave_ctr != nullptr && wave > 0) {  // lock-step waves, bounded wait
+          target += 2u * static_cast<uint32_t>(min(npairs, num_tiles - wave * npairs));
+          atomicAdd(wave_ctr, 1u);
+          uint32_t v;
+          for (int spin = 0; spin < 2000; ++spin) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(wave_ctr) : "memory");
+            if (v >= target) break;
+            __nanosleep(100);
+          }
+        }
+        int tm, tn;
+        grouped_tile(tile, tiles_m, tiles_n, shp.group_m, tm, tn);
+        const int m_cta = tm * 2 * C::BM + rank * C::BM;
+        const int n_cta = tn * C::BN + rank * C::BN_CTA;
+        for (int kb = 0; kb < nop; ++kb, ++g) {
+          const int o = g % C::NOP;
+          sm100::mbar_wait(&op_empty[o], ((g / C::NOP) & 1) ^ 1);
+          if (rank == 0) sm100::mbar_arrive_expect_tx(&op_full[o], 2 * C::OP_BYTES);
+          const uint32_t dst = smem_base + C::OFF_OP + o * C::OP_BYTES;
+          const uint32_t bar = leader_full + o * 8;
+          const int kc = kb * VC::BK_OP;
+          tma_load_2d_pair(dst + C::OFF_AHI, &tmAh, bar, kc, m_cta);
+          tma_load_2d_pair(dst + C::OFF_BHI, &tmBh, bar, kc, n_cta);
+          if constexpr (C::kLo) {
+            tma_load_2d_pair(dst + C::OFF_ALO, &tmAl, bar, kc, m_cta);
+            tma_load_2d_pair(dst + C::OFF_BLO, &tmBl, bar, kc, n_cta);
+          }
         }
       }
     } else if (warp == 1 && lane == 0 && rank == 0) {
       // ===================== MMA issuer (leader CTA) =====================
       constexpr uint32_t idesc = sm100::umma_idesc(VC::AB_FORMAT, 2 * C::BM, C::BN);
       constexpr uint32_t hi_w = (1024u >> 4) | (1u << 14) | (2u << 29);  // SBO 1024, v1, SW128
-      for (int kb = 0; kb < nop; ++kb) {
-        const int o = kb % C::NOP;
-        sm100::mbar_wait(&op_full[o], (kb / C::NOP) & 1);
-        sm100::tc_fence_after();
-        const uint32_t op = sm100::opaque(smem_base + C::OFF_OP + o * C::OP_BYTES) >> 4;
-        const uint32_t ahi = op | (1u << 16);
-        const uint32_t alo = ahi + (C::OFF_ALO >> 4);
-        const uint32_t bhi = ahi + (C::OFF_BHI >> 4);
-        const uint32_t blo = ahi + (C::OFF_BLO >> 4);
-        if constexpr (S == kSchPlain) {
-#pragma unroll
-          for (int ks = 0; ks < 4; ++ks)
-            sm100::mma_pair_split<V == kTF32>(tmem_P, ahi + 2 * ks, hi_w, bhi + 2 * ks, hi_w, idesc,
-                                              (kb | ks) != 0);
-        } else if constexpr (S == kSchIn4) {
-          // the reference's four-call order per block: dA*dB, dA*B, A*dB, A*B
-#pragma unroll
-          for (int ks = 0; ks < 4; ++ks) {
-            sm100::mma_pair_split<V == kTF32>(tmem_P, alo + 2 * ks, hi_w, blo + 2 * ks, hi_w, idesc,
-                                              (kb | ks) != 0);
-            sm100::mma_pair_split<V == kTF32>(tmem_P, alo + 2 * ks, hi_w, bhi + 2 * ks, hi_w, idesc, 1u);
-            sm100::mma_pair_split<V == kTF32>(tmem_P, ahi + 2 * ks, hi_w, blo + 2 * ks, hi_w, idesc, 1u);
-            sm100::mma_pair_split<V == kTF32>(tmem_P, ahi + 2 * ks, hi_w, bhi + 2 * ks, hi_w, idesc, 1u);
-          }
-        } else {
-          // corrections first (reference order per k-step: dA*B then A*dB), so the
-          // drain of the previous P overlaps them (schemes.py:294-298)
-#pragma unroll
-          for (int ks = 0; ks < 4; ++ks) {
-            sm100::mma_pair_split<V == kTF32>(tmem_dC, alo + 2 * ks, hi_w, bhi + 2 * ks, hi_w, idesc,
-                                              (kb | ks) != 0);
-            sm100::mma_pair_split<V == kTF32>(tmem_dC, ahi + 2 * ks, hi_w, blo + 2 * ks, hi_w, idesc, 1u);
-            if constexpr (S == kSchC3DD)  // schemes.py:308-313: the dA*dB chain
-              sm100::mma_pair_split<V == kTF32>(tmem_ddC, alo + 2 * ks, hi_w, blo + 2 * ks, hi_w, idesc,
-                                                (kb | ks) != 0);
-          }
-          const bool first_in_interval = (kb % de) == 0;
-          if (first_in_interval && kb > 0) {
-            sm100::mbar_wait_cluster(p_empty, ((kb / de) - 1) & 1);
+      uint32_t g = 0, git = 0, gtile = 0;
+      for (int tile = pid; tile < num_tiles; tile += npairs, ++gtile) {
+        for (int kb = 0; kb < nop; ++kb, ++g) {
+          const int o = g % C::NOP;
+          sm100::mbar_wait(&op_full[o], (g / C::NOP) & 1);
+          sm100::tc_fence_after();
+          if (kb == 0 && gtile > 0) {  // the previous tile's epilogue has read the accumulators
+            sm100::mbar_wait_cluster(acc_empty, (gtile - 1) & 1);
             sm100::tc_fence_after();
           }
+          const uint32_t op = sm100::opaque(smem_base + C::OFF_OP + o * C::OP_BYTES) >> 4;
+          const uint32_t ahi = op | (1u << 16);
+          const uint32_t alo = ahi + (C::OFF_ALO >> 4);
+          const uint32_t bhi = ahi + (C::OFF_BHI >> 4);
+          const uint32_t blo = ahi + (C::OFF_BLO >> 4);
+          if constexpr (S == kSchPlain) {
 #pragma unroll
-          for (int ks = 0; ks < 4; ++ks)
-            sm100::mma_pair_split<V == kTF32>(tmem_P, ahi + 2 * ks, hi_w, bhi + 2 * ks, hi_w, idesc,
-                                              !(first_in_interval && ks == 0));
+            for (int ks = 0; ks < 4; ++ks)
+              sm100::mma_pair_split<V == kTF32>(tmem_P, ahi + 2 * ks, hi_w, bhi + 2 * ks, hi_w, idesc,
+                                                (kb | ks) != 0);
+          } else if constexpr (S == kSchIn4) {
+            // the reference's four-call order per block: dA*dB, dA*B, A*dB, A*B
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {
+              sm100::mma_pair_split<V == kTF32>(tmem_P, alo + 2 * ks, hi_w, blo + 2 * ks, hi_w, idesc,
+                                                (kb | ks) != 0);
+              sm100::mma_pair_split<V == kTF32>(tmem_P, alo + 2 * ks, hi_w, bhi + 2 * ks, hi_w, idesc, 1u);
+              sm100::mma_pair_split<V == kTF32>(tmem_P, ahi + 2 * ks, hi_w, blo + 2 * ks, hi_w, idesc, 1u);
+              sm100::mma_pair_split<V == kTF32>(tmem_P, ahi + 2 * ks, hi_w, bhi + 2 * ks, hi_w, idesc, 1u);
+            }
+          } else {
+            // corrections first (reference order per k-step: dA*B then A*dB), so the
+            // drain of the previous P overlaps them (schemes.py:294-298)
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {
+              sm100::mma_pair_split<V == kTF32>(tmem_dC, alo + 2 * ks, hi_w, bhi + 2 * ks, hi_w, idesc,
+                                                (kb | ks) != 0);
+              sm100::mma_pair_split<V == kTF32>(tmem_dC, ahi + 2 * ks, hi_w, blo + 2 * ks, hi_w, idesc, 1u);
+              if constexpr (S == kSchC3DD)  // schemes.py:308-313: the dA*dB chain
+                sm100::mma_pair_split<V == kTF32>(tmem_ddC, alo + 2 * ks, hi_w, blo + 2 * ks, hi_w,
+                                                  idesc, (kb | ks) != 0);
+            }
+            const bool first_in_interval = (kb % de) == 0;
+            if (first_in_interval && git > 0) {
+              sm100::mbar_wait_cluster(p_empty, (git - 1) & 1);
+              sm100::tc_fence_after();
+            }
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks)
+              sm100::mma_pair_split<V == kTF32>(tmem_P, ahi + 2 * ks, hi_w, bhi + 2 * ks, hi_w, idesc,
+                                                !(first_in_interval && ks == 0));
+          }
+          sm100::mma_commit_pair_mc(&op_empty[o], 0x3);
+          if (kb == nop - 1 || (C::kDrain && (kb % de) == de - 1)) {
+            sm100::mma_commit_pair_mc(p_full, 0x3);
+            ++git;
+          }
         }
-        sm100::mma_commit_pair_mc(&op_empty[o], 0x3);
-        if (kb == nop - 1 || (C::kDrain && (kb % de) == de - 1))
-          sm100::mma_commit_pair_mc(p_full, 0x3);
       }
     }
   } else {
@@ -340,76 +361,80 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PsCfg<V, S>::NUM_THR
     const int h = (warp - C::DRAIN_WARP0) >> 2;
     const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
     const uint32_t p_empty_leader = sm100::mapa_shared(sm100::smem_u32(p_empty), 0);
+    const uint32_t acc_empty_leader = sm100::mapa_shared(sm100::smem_u32(acc_empty), 0);
     constexpr int NC = C::DRAIN_COLS;
-    float acc[NC];
-#pragma unroll
-    for (int j = 0; j < NC; ++j) acc[j] = 0.0f;
-    for (int it = 0; it < nintervals; ++it) {
-      sm100::mbar_wait(p_full, it & 1);
-      sm100::tc_fence_after();
-#pragma unroll
-      for (int c = 0; c < NC / 16; ++c) {
-        uint32_t r[16];
-        sm100::tmem_ld_32x32b_x16(tmem_P + lane_off + h * NC + c * 16, r);
-        sm100::tmem_ld_wait();
-#pragma unroll
-        for (int j = 0; j < 16; j += 2)  // schemes.py:300-304: c = RN32(c + partial), f32x2
-          sm100::fadd2_rn(acc[c * 16 + j], acc[c * 16 + j + 1], __uint_as_float(r[j]),
-                          __uint_as_float(r[j + 1]));
-      }
-      sm100::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) sm100::mbar_arrive_remote(p_empty_leader);
-    }
-    if constexpr (!C::kDrain) {
-      // in-unit schemes: the single accumulator is the result
-      sm100::mbar_wait(p_full, 0);
-      sm100::tc_fence_after();
-    }
     bool nonfinite = false;
-    const uint32_t stage = smem_base + (warp - C::DRAIN_WARP0) * C::EPI_WARP_BYTES;
+    uint32_t git = 0;
+    for (int tile = pid; tile < num_tiles; tile += npairs) {
+      int tm, tn;
+      grouped_tile(tile, tiles_m, tiles_n, shp.group_m, tm, tn);
+      float acc[NC];
 #pragma unroll
-    for (int b = 0; b < NC / 32; ++b) {
-      const uint32_t box = stage + b * 4096;
+      for (int j = 0; j < NC; ++j) acc[j] = 0.0f;
+      for (int it = 0; it < nintervals; ++it, ++git) {
+        sm100::mbar_wait(p_full, git & 1);
+        sm100::tc_fence_after();
+        if constexpr (C::kDrain) {
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const uint32_t col = lane_off + h * NC + b * 32 + c * 16;
-        uint32_t r[16];
-        sm100::tmem_ld_32x32b_x16((C::kDrain ? tmem_dC : tmem_P) + col, r);
+          for (int c = 0; c < NC / 8; ++c) {
+            uint32_t r[8];
+            sm100::tmem_ld_32x32b_x8(tmem_P + lane_off + h * NC + c * 8, r);
+            sm100::tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 8; j += 2)  // schemes.py:300-304: c = RN32(c + partial), f32x2
+              sm100::fadd2_rn(acc[c * 8 + j], acc[c * 8 + j + 1], __uint_as_float(r[j]),
+                              __uint_as_float(r[j + 1]));
+          }
+          sm100::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) sm100::mbar_arrive_remote(p_empty_leader);
+        }
+      }
+      // epilogue: every MMA of the tile has completed (its last p_full follows them)
+      const int64_t row = static_cast<int64_t>(tm) * 2 * C::BM + rank * C::BM + q * 32 + lane;
+      const int col0 = tn * C::BN + h * NC;
+      float* crow = Cout + row * ldc + col0;
+#pragma unroll
+      for (int c = 0; c < NC / 8; ++c) {
+        uint32_t r[8];
+        sm100::tmem_ld_32x32b_x8((C::kDrain ? tmem_dC : tmem_P) + lane_off + h * NC + c * 8, r);
         sm100::tmem_ld_wait();
-        uint32_t rr[16];
+        uint32_t rr[8];
         if constexpr (S == kSchC3DD) {
-          sm100::tmem_ld_32x32b_x16(tmem_ddC + col, rr);
+          sm100::tmem_ld_32x32b_x8(tmem_ddC + lane_off + h * NC + c * 8, rr);
           sm100::tmem_ld_wait();
         }
-        float o[16];
+        float o[8];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
+        for (int j = 0; j < 8; ++j) {
           if constexpr (C::kDrain) {
             // schemes.py:306-307: one rounding of c + dC * 2^-s
-            o[j] = __fmaf_rn(__uint_as_float(r[j]), inv_scale, acc[b * 32 + c * 16 + j]);
+            o[j] = __fmaf_rn(__uint_as_float(r[j]), inv_scale, acc[c * 8 + j]);
             if constexpr (S == kSchC3DD)  // schemes.py:312-313: then + ddC * 2^-2s
               o[j] = __fmaf_rn(__uint_as_float(rr[j]), inv_scale2, o[j]);
           } else {
             o[j] = __uint_as_float(r[j]);
           }
-          nonfinite |= !isfinite(o[j]);
+          nonfinite |= !isfinite(o[j]) && row < shp.m && col0 + c * 8 + j < shp.n;
         }
+        if (row < shp.m) {
+          const int col = col0 + c * 8;
+          if (col + 8 <= shp.n) {
+            *reinterpret_cast<float4*>(crow + c * 8) = make_float4(o[0], o[1], o[2], o[3]);
+            *reinterpret_cast<float4*>(crow + c * 8 + 4) = make_float4(o[4], o[5], o[6], o[7]);
+          } else {
 #pragma unroll
-        for (int v = 0; v < 4; ++v)
-          sm100::sts128f(box + sw128(lane, c * 4 + v), o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
+            for (int j = 0; j < 8; ++j)
+              if (col + j < shp.n) crow[c * 8 + j] = o[j];
+          }
+        }
       }
-      sm100::fence_proxy_async_smem();
+      sm100::tc_fence_before();
       __syncwarp();
-      if (lane == 0) {
-        sm100::tma_store_2d(&tmC, smem + (box - smem_base), n_pair + h * NC + b * 32, m_cta + q * 32);
-        sm100::tma_store_commit();
-      }
+      if (lane == 0) sm100::mbar_arrive_remote(acc_empty_leader);
     }
-    if (lane == 0) sm100::tma_store_wait0();
     if (flags != nullptr && __any_sync(0xFFFFFFFFu, nonfinite) && lane == 0)
       atomicOr(flags, kFlagOverflow);
-    sm100::tc_fence_before();
   }
 
   __syncthreads();
