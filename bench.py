@@ -53,6 +53,9 @@ def parse():
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--variant", choices=["tf32", "fp16"], default="tf32")
     p.add_argument("--n", type=int, default=16384)
+    p.add_argument("--m-total", type=int, default=0,
+                   help="strong scaling: total rows of A / C split over the ranks "
+                        "(BASELINE configs[4]: --m-total 65536 --n 65536); default: n rows per rank")
     p.add_argument("--allgather", action="store_true")
     p.add_argument("--overlap-chunks", type=int, default=1,
                    help="with --allgather: all-gather row chunks while the next chunk computes")
@@ -225,25 +228,26 @@ def main():
     torch.set_float32_matmul_precision("highest")
 
     n = args.n
+    mr = -(-args.m_total // world) if args.m_total > 0 else n  # rows of A / C on this rank
     scheme = SCHEME[args.variant]
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
-    A = (torch.rand((n, n), generator=gen, device=dev) * 2 - 1).contiguous()
+    A = (torch.rand((mr, n), generator=gen, device=dev) * 2 - 1).contiguous()
     gen.manual_seed(99)  # B replicated: identical on every rank
     B = (torch.rand((n, n), generator=gen, device=dev) * 2 - 1).contiguous()
-    C = torch.empty((n, n), device=dev)
-    Cfull = torch.empty((n * world, n), device=dev) if (args.allgather and world > 1) else None
+    C = torch.empty((mr, n), device=dev)
+    Cfull = torch.empty((mr * world, n), device=dev) if (args.allgather and world > 1) else None
     stream = torch.cuda.current_stream(dev)
-    flops_step = 2.0 * n * n * n  # per rank
+    flops_step = 2.0 * mr * n * n  # per rank
 
     from paper_2203_03341_b200.sharded import sharded_gemm, sharded_gemm_fused
 
     def step():
         if Cfull is not None and args.fused_allgather:
-            sharded_gemm_fused(A, B, scheme, m_total=n * world)
+            sharded_gemm_fused(A, B, scheme, m_total=mr * world)
             return
         if Cfull is not None and args.overlap_chunks > 1:
-            sharded_gemm(A, B, scheme, m_total=n * world, allgather=True,
+            sharded_gemm(A, B, scheme, m_total=mr * world, allgather=True,
                          overlap_chunks=args.overlap_chunks)
             return
         T.gemm_device(A, B, scheme, out=C)
@@ -303,16 +307,19 @@ def main():
                               f"dense = {peak_basis} bf16 burst {bf16:.1f} TF/s"
                               + ("" if args.variant == "fp16" else " / 2 (TF32 rate)"),
                 "algorithmic_flops_per_launch": flops_step,
-                "algorithmic_bytes_per_launch": 4.0 * 3 * n * n}
+                "algorithmic_bytes_per_launch": 4.0 * (2 * mr * n + n * n)}
 
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": "strong" if args.m_total > 0 else "weak",
+        "vs_baseline": None, "dtype": "f32",
         "data": "synthetic urand(-1,1) FP32 (torch Philox on device)",
-        "config": {"workload": f"{'TF32' if args.variant == 'tf32' else 'FP16'}-TCEC SGEMM "
-                               f"m=n=k={n} per rank" + (", row-sharded" if world > 1 else ""),
-                   "variant": args.variant, "scheme": scheme, "m": n * world, "n": n, "k": n,
+        "config": {"workload": (f"{'TF32' if args.variant == 'tf32' else 'FP16'}-TCEC SGEMM "
+                                + (f"m={mr * world} n=k={n}, {mr} rows per rank" if args.m_total > 0
+                                   else f"m=n=k={n} per rank")
+                                + (", row-sharded" if world > 1 else "")),
+                   "variant": args.variant, "scheme": scheme, "m": mr * world, "n": n, "k": n,
                    "parallelism": f"row-shard x{world}" + (
                        (" + fused all-gather C (epilogue peer stores)" if args.fused_allgather
                         else " + all-gather C") if Cfull is not None else ""),
@@ -401,13 +408,13 @@ def main():
     if not args.no_e2e:
         del C
         torch.cuda.empty_cache()
-        hA = torch.empty((n, n), dtype=torch.float32, pin_memory=True)
+        hA = torch.empty((mr, n), dtype=torch.float32, pin_memory=True)
         hB = torch.empty((n, n), dtype=torch.float32, pin_memory=True)
         hA.copy_(A)
         hB.copy_(B)
         del A, B
         torch.cuda.empty_cache()
-        hC = torch.empty((n, n), dtype=torch.float32, pin_memory=True)
+        hC = torch.empty((mr, n), dtype=torch.float32, pin_memory=True)
         npA, npB, npC = hA.numpy(), hB.numpy(), hC.numpy()
         e2e_steps = max(2, min(args.steps, 5))
         T.gemm(npA, npB, scheme, out=npC)  # warm-up (pool, descriptors)
@@ -423,7 +430,7 @@ def main():
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         dt = float(tt.item())
         line["e2e"] = {"value": world * flops_step / dt / 1e12, "unit": "TFLOP/s",
-                       "h2d_bytes_per_step": 2 * n * n * 4, "d2h_bytes_per_step": n * n * 4,
+                       "h2d_bytes_per_step": (mr * n + n * n) * 4, "d2h_bytes_per_step": mr * n * 4,
                        "ms_per_step": dt * 1e3,
                        "path": "paper_2203_03341_b200.gemm(numpy pinned) -> tcec_sgemm_host"}
         del run
