@@ -733,3 +733,32 @@ def test_lockstep_kernel_in_cuda_graph_and_concurrent_streams():
     torch.cuda.synchronize()
     for o in outs:
         assert torch.equal(o, ref)
+
+
+@pytest.mark.parametrize("case", range(24))
+def test_randomized_shapes_and_ranges_vs_oracle(case):
+    """Seeded fuzz over shapes (1..700 rows / columns, 1..1500 k, ragged in every
+    dimension), exponent ranges (urand and ExpRand bands inside the FP16 range
+    and, for TF32, across 2^-100..2^60), both variants and the default kernel
+    selection: the GPU result is within the GEMM tolerance of the oracle with
+    the same drain interval, with identical flags."""
+    rng = np.random.default_rng(1000 + case)
+    m, n = (int(x) for x in rng.integers(1, 700, 2))
+    k = int(rng.integers(1, 1500))
+    variant = "fp16" if case % 2 == 0 else "tf32"
+    sname, bk, drain = ("corrected3_halfhalf", 16, 128) if variant == "fp16" else ("corrected3_tf32", 8, 64)
+    kind = case % 3
+    if kind == 0:
+        a = O.urand(m, k, -1, 1, 3 * case)
+        b = O.urand(k, n, -1, 1, 3 * case + 1)
+    elif kind == 1:
+        a = O.exprand(m, k, -14, 14, 3 * case)
+        b = O.exprand(k, n, -14, 14, 3 * case + 1)
+    else:
+        lo, hi = (-20, 12) if variant == "fp16" else (-100, 60)
+        a = O.exprand(m, k, lo, hi, 3 * case)
+        b = O.exprand(k, n, lo, hi, 3 * case + 1)
+    c, fl = _run(a, b, sname)
+    oc, ofl = O.corrected3(a, b, variant, block_k=bk, drain_k=drain)
+    assert (fl.saw_overflow, fl.saw_out_of_range) == (bool(ofl & 1), bool(ofl & 2)), case
+    _check_close(c, oc, a, b, sname, variant, out_of_range=bool(ofl & 2))
