@@ -120,3 +120,23 @@ def test_torch_op_registered_with_fake_impl():
     assert c.shape == (64, 48) and fl.dtype == torch.int32
     with pytest.raises(Exception):
         torch.ops.tcec.sgemm(torch.zeros(4, 4), torch.zeros(4, 4), 1, 0)
+
+
+def test_c_example_builds_against_the_header_and_library():
+    """examples/tcec_example.c -- a plain C caller of include/tcec.h linked
+    against the in-tree libtcec.so -- compiles and links (runs in the GPU suite)."""
+    import subprocess
+
+    subprocess.run(["make", "-s", "-B", "-C", os.path.join(ROOT, "examples")], check=True)
+    assert os.path.exists(os.path.join(ROOT, "examples", "tcec_example"))
+
+
+@pytest.mark.gpu
+def test_c_example_runs():
+    import subprocess
+
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "examples")], check=True)
+    out = subprocess.run([os.path.join(ROOT, "examples", "tcec_example"), "512"], capture_output=True,
+                         text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "relres" in out.stdout
