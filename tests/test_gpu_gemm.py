@@ -762,3 +762,26 @@ def test_randomized_shapes_and_ranges_vs_oracle(case):
     oc, ofl = O.corrected3(a, b, variant, block_k=bk, drain_k=drain)
     assert (fl.saw_overflow, fl.saw_out_of_range) == (bool(ofl & 1), bool(ofl & 2)), case
     _check_close(c, oc, a, b, sname, variant, out_of_range=bool(ofl & 2))
+
+
+def test_strided_and_transposed_views_match_contiguous():
+    """gemm_device accepts any 2-D CUDA float32 view (transposed, sliced with an
+    odd leading dimension, offset by one element): operands that are not
+    TMA-ready are copied once, and the result equals the contiguous call."""
+    import torch
+
+    T = _T()
+    g = torch.Generator(device="cuda")
+    g.manual_seed(13)
+    base_a = torch.rand((301, 517), generator=g, device="cuda") * 2 - 1
+    base_b = torch.rand((517, 263), generator=g, device="cuda") * 2 - 1
+    views = [
+        (base_a, base_b),
+        (base_a.t().contiguous().t(), base_b),          # column-major A
+        (base_a[:, 1:], base_b[1:, :]),                  # odd offset / leading dimension
+        (base_a[::2], base_b),                           # row stride 2 * 517
+    ]
+    for a, b in views:
+        ref = T.gemm_device(a.contiguous(), b.contiguous(), "corrected3_tf32")
+        out = T.gemm_device(a, b, "corrected3_tf32")
+        assert torch.equal(out, ref)
