@@ -2,8 +2,9 @@
 //
 // The fused kernels (tcec_gemm2.cuh) re-split every A tile once per column
 // tile of C and every B tile once per row tile (n / 256 and m / 256 times at
-// 16384^3), and on B200 that redundant split -- its FP32 staging writes and
-// reads through shared memory -- is what bounds them.  This mode
+// 16384^3), and on the power-capped B200 the energy of that redundant split
+// (FP32 staging through shared memory, split arithmetic, hi/lo stores) is what
+// bounds the FP16 variant.  This mode
 // splits each input element exactly once in an HBM-bandwidth-bound pass and
 // then runs a plain three-product tcgen05 GEMM whose TMA loads the hi / lo
 // operands straight into the UMMA layout:
@@ -11,10 +12,12 @@
 //   tcec_presplit_kernel   X (FP32) -> hi, lo in the operand element type (FP16
 //                          or TF32 bit patterns), K-major: A as m x k, B
 //                          transposed to n x k; RunFlags from the same pass.
-//   tcec_gemm_ps_kernel    CTA pair, 256 x 256 tile, 3-deep ring of 64 KB
-//                          operand stages (A_hi, A_lo, B_hi, B_lo; 128-byte
-//                          swizzled K-major), the same MMA order, drain and
-//                          epilogue as the fused pair kernel -- bit-identical C.
+//   tcec_gemm_ps_kernel    persistent CTA pair (lock-step waves as in
+//                          tcec_gemm5.cuh), 256 x 256 tiles, 3-deep ring of
+//                          64 KB operand stages (A_hi, A_lo, B_hi, B_lo;
+//                          128-byte swizzled K-major), the same MMA order and
+//                          drain as the fused pair kernel, C stored from
+//                          registers -- bit-identical C.
 //
 // Split arithmetic is split.cuh's (splitting.py:114-122), including lo = 0
 // where hi overflowed.
