@@ -44,11 +44,19 @@ extern "C" {
  *                  converted RN (FP16) / RNA (TF32) (schemes.py:343-351)
  *   INUNIT4        markidis4 / corrected4 with the hardware's terminal
  *                  rounding: four products in one accumulator, unscaled split
- *                  (schemes.py:99-117, :352-364)  */
+ *                  (schemes.py:99-117, :352-364)
+ *   INUNIT4_RN     corrected4_rn: the same four products with an RN terminal,
+ *                  emulated: each product accumulates one block of drain_k
+ *                  in its own tensor-memory accumulator, and the blocks are
+ *                  added in term order into an FP32 round-to-nearest sum on
+ *                  the CUDA cores (mma.py:84-85).  drain_k is the reference's
+ *                  block_k here: 0 = 16, else a multiple of the MMA k-step
+ *                  (16 FP16, 8 TF32).  */
 #define TCEC_SCHEME_CORRECTED3 0
 #define TCEC_SCHEME_CORRECTED3_DD 1
 #define TCEC_SCHEME_TC_PLAIN 2
 #define TCEC_SCHEME_INUNIT4 3
+#define TCEC_SCHEME_INUNIT4_RN 4
 
 /* Status codes. */
 #define TCEC_OK 0
@@ -66,7 +74,8 @@ typedef struct tcec_opts {
   int32_t scale_log2;
   /* Drain interval of the main-term partial in k (MmaConfig.block_k,
    * mma.py:34): 0 = default (128 for FP16, 64 for TF32); otherwise a positive
-   * multiple of the operand stage depth (64 for FP16, 32 for TF32). */
+   * multiple of the operand stage depth (64 for FP16, 32 for TF32).
+   * TCEC_SCHEME_INUNIT4_RN: the block of each drained product (see above). */
   int32_t drain_k;
   /* Output tile width: 0 = default (256: CTA-pair 256 x 256 tile); 128 = single-CTA 128 x 128;
    * 192 = CTA-pair 256 x 192 tile with the split A operand in tensor memory. */

@@ -122,10 +122,11 @@ def corrected3(a, b, variant: str = "fp16", block_k: int = 16, drain_k: int | No
 def inunit(a, b, scheme: str, block_k: int = 16, acc_bits: int = 25):
     """schemes.py:gemm for the in-unit comparators restated (tcec_oracle_inunit):
     scheme in tc_plain_fp16, tc_plain_tf32, markidis4, markidis4_tf32,
-    corrected4_rn, corrected4_rz.  Returns (C float32, flags int)."""
+    corrected4_rn, corrected4_rz, corrected4_rn_tf32 (RN terminal, TF32 split).  Returns (C float32, flags int)."""
     kinds = {"tc_plain_fp16": (0, 0, 0, 0, 2), "tc_plain_tf32": (0, 1, 0, 1, 2),
              "markidis4": (1, 0, 0, 0, 2), "markidis4_tf32": (1, 1, 0, 1, 2),
-             "corrected4_rn": (1, 0, 0, 0, 0), "corrected4_rz": (1, 0, 0, 0, 2)}
+             "corrected4_rn": (1, 0, 0, 0, 0), "corrected4_rz": (1, 0, 0, 0, 2),
+             "corrected4_rn_tf32": (1, 1, 0, 1, 0)}
     kind, fmt, s, rm, term = kinds[scheme]
     a = np.ascontiguousarray(a, dtype=np.float32)
     b = np.ascontiguousarray(b, dtype=np.float32)

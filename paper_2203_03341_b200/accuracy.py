@@ -32,7 +32,7 @@ import numpy as np
 from .genmat import ExpRand, MatrixSpec, Urand, generate, pair_seed, type_pair
 
 GPU_SCHEMES = ("corrected3_halfhalf", "corrected3_tf32", "tc_plain_fp16", "tc_plain_tf32",
-               "markidis4", "corrected4_rz", "cublas_sgemm")
+               "markidis4", "corrected4_rz", "corrected4_rn", "cublas_sgemm")
 
 
 def _fmt64(x: float) -> str:

@@ -400,6 +400,8 @@ int dispatch_bn(int bn, int64_t m, int64_t n, int64_t k, const float* A, int64_t
         return launch_gemm_presplit<V, R, tcec::kSchPlain>(m, n, k, A, lda, B, ldb, C, ldc, 0, de, g, gm_user, ls, fl, st);
       case TCEC_SCHEME_INUNIT4:
         return launch_gemm_presplit<V, R, tcec::kSchIn4>(m, n, k, A, lda, B, ldb, C, ldc, s, de, g, gm_user, ls, fl, st);
+      case TCEC_SCHEME_INUNIT4_RN:  // de = MMA k-steps per drained block
+        return launch_gemm_presplit<V, R, tcec::kSchIn4RN>(m, n, k, A, lda, B, ldb, C, ldc, s, de, g, gm_user, ls, fl, st);
       default:
         return TCEC_ERR_UNSUPPORTED;
     }
@@ -511,7 +513,8 @@ int sgemm_impl(int variant, int64_t m, int64_t n, int64_t k, const float* A, int
   if (opts) o = *opts;
   const int rounding = resolve_rounding(variant, o.split_rounding);
   if (!rounding_supported(variant, rounding)) return TCEC_ERR_UNSUPPORTED;
-  int scale_log2 = o.scale_log2 < 0 ? (variant == TCEC_FP16 && o.scheme != TCEC_SCHEME_INUNIT4 &&
+  const bool in_unit = o.scheme == TCEC_SCHEME_INUNIT4 || o.scheme == TCEC_SCHEME_INUNIT4_RN;
+  int scale_log2 = o.scale_log2 < 0 ? (variant == TCEC_FP16 && !in_unit &&
                                         o.scheme != TCEC_SCHEME_TC_PLAIN ? 11 : 0)
                                      : o.scale_log2;
   if (variant == TCEC_TF32 && scale_log2 != 0) return TCEC_ERR_UNSUPPORTED;
@@ -520,7 +523,13 @@ int sgemm_impl(int variant, int64_t m, int64_t n, int64_t k, const float* A, int
   // default drain interval: 128 (FP16) / 64 (TF32) -- measured both faster and
   // more accurate against FP64 than draining every operand stage
   int drain_every = 2;
-  if (o.drain_k != 0) {
+  if (o.scheme == TCEC_SCHEME_INUNIT4_RN) {
+    // the drained block is the reference's block_k, in MMA k-steps (16 / 8 deep)
+    const int kstep = variant == TCEC_FP16 ? 16 : 8;
+    const int bk = o.drain_k == 0 ? 16 : o.drain_k;
+    if (bk < 0 || bk % kstep != 0) return TCEC_ERR_UNSUPPORTED;
+    drain_every = bk / kstep;
+  } else if (o.drain_k != 0) {
     if (o.drain_k < 0 || o.drain_k % bk_op != 0) return TCEC_ERR_UNSUPPORTED;
     drain_every = o.drain_k / bk_op;
   }
@@ -541,8 +550,8 @@ int sgemm_impl(int variant, int64_t m, int64_t n, int64_t k, const float* A, int
   if (split_mode < 0 || split_mode > 2) return TCEC_ERR_UNSUPPORTED;
   // scheme: product schedule (TCEC_SCHEME_*); the comparators run in split-once mode
   const int scheme = o.scheme;
-  if (scheme < TCEC_SCHEME_CORRECTED3 || scheme > TCEC_SCHEME_INUNIT4) return TCEC_ERR_UNSUPPORTED;
-  if (scheme == TCEC_SCHEME_INUNIT4 && o.scale_log2 > 0) return TCEC_ERR_UNSUPPORTED;
+  if (scheme < TCEC_SCHEME_CORRECTED3 || scheme > TCEC_SCHEME_INUNIT4_RN) return TCEC_ERR_UNSUPPORTED;
+  if (in_unit && o.scale_log2 > 0) return TCEC_ERR_UNSUPPORTED;
   if (m == 0 || n == 0) return TCEC_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (k == 0) {

@@ -154,12 +154,18 @@ __global__ void __launch_bounds__(256)
 //             the unit over all k                    (schemes.py:343-351)
 //   kSchIn4   markidis4 / corrected4 (hardware terminal): dA*dB, dA*B, A*dB,
 //             A*B per k-step into one accumulator    (schemes.py:352-364)
-enum Schedule : int { kSchC3 = 0, kSchC3DD = 1, kSchPlain = 2, kSchIn4 = 3 };
+//   kSchIn4RN corrected4 with the RN terminal (schemes.py:352-364, terminal RN):
+//             the same four terms, each in its own TMEM accumulator over one
+//             block of `drain_every` MMA k-steps, drained in the reference's
+//             term order into an FP32 RN register sum -- c = RN(c + P_t) per
+//             block and term (mma.py:84-85), the CUDA-core add standing in for
+//             an RN terminal the tensor core does not have
+enum Schedule : int { kSchC3 = 0, kSchC3DD = 1, kSchPlain = 2, kSchIn4 = 3, kSchIn4RN = 4 };
 
 template <int V, int S = kSchC3>
 struct PsCfg {
   static constexpr int BM = 128;                         // rows per CTA (pair M = 256)
-  static constexpr int BN = S == kSchC3DD ? 128 : 256;   // pair N (3 accumulators need N <= 170)
+  static constexpr int BN = S == kSchC3DD || S == kSchIn4RN ? 128 : 256;  // 3-4 accumulators: N <= 128
   static constexpr int BN_CTA = BN / 2;                  // B rows (= C columns) loaded per CTA
   static constexpr int A_TILE = 128 * 128;               // 128 rows x 128-byte k chunk
   static constexpr int B_TILE = BN_CTA * 128;
@@ -172,10 +178,11 @@ struct PsCfg {
   static constexpr int NOP = (192 * 1024) / OP_BYTES;    // 3 / 4 / 6 stages
   static constexpr int OFF_OP = 0;
   static constexpr int OFF_BAR = NOP * OP_BYTES;
-  static constexpr int NUM_BARS = 2 * NOP + 2;
+  static constexpr int NUM_PE = S == kSchIn4RN ? 4 : 1;  // p_empty barriers (one per drained P)
+  static constexpr int NUM_BARS = 2 * NOP + 1 + NUM_PE;
   static constexpr int SMEM_BYTES = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr bool kDrain = S == kSchC3 || S == kSchC3DD;
-  static constexpr int NUM_ACC = S == kSchC3 ? 2 : (S == kSchC3DD ? 3 : 1);
+  static constexpr int NUM_ACC = S == kSchC3 ? 2 : (S == kSchC3DD ? 3 : (S == kSchIn4RN ? 4 : 1));
   static constexpr int TMEM_COLS = NUM_ACC * BN > 256 ? 512 : 256;  // P | dC | ddC
   static constexpr int NUM_THREADS = 384;                // warps 0-3 control, 4-11 drain
   static constexpr int DRAIN_WARP0 = 4, NUM_DRAIN_WARPS = 8;
@@ -217,7 +224,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PsCfg<V, S>::NUM_THR
   uint64_t* op_full = bars;                 // TMA (both CTAs) -> MMA   (leader, tx)
   uint64_t* op_empty = bars + C::NOP;       // MMA commit -> TMA        (both, multicast)
   uint64_t* p_full = bars + 2 * C::NOP;     // MMA commit -> drain      (both, multicast)
-  uint64_t* p_empty = p_full + 1;           // drain -> MMA             (leader, 16)
+  uint64_t* p_empty = p_full + 1;           // drain -> MMA             (leader, 16; one per P)
   uint64_t* acc_empty = bars + C::NUM_BARS; // epilogue -> next tile's MMA (leader, 16)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NUM_BARS + 1);
   const uint32_t smem_base = sm100::smem_u32(smem);
@@ -232,7 +239,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PsCfg<V, S>::NUM_THR
   const int pid = blockIdx.x >> 1;
   const int nop = shp.num_op_stages;
   const int de = shp.drain_every;
-  const int nintervals = C::kDrain ? (nop + de - 1) / de : 1;
+  // drain intervals per tile: op-stage groups (corrected3), blocks of `de` MMA
+  // k-steps (4 per op stage) for kSchIn4RN, else one (the epilogue)
+  const int nintervals = C::kDrain ? (nop + de - 1) / de
+                                   : (S == kSchIn4RN ? (4 * nop + de - 1) / de : 1);
 
   if (warp == 0 && lane == 0) {
     if (smem_base & 1023u) __trap();
@@ -245,7 +255,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PsCfg<V, S>::NUM_THR
       sm100::mbar_init(&op_empty[o], 1);
     }
     sm100::mbar_init(p_full, 1);
-    sm100::mbar_init(p_empty, 2 * C::NUM_DRAIN_WARPS);
+    for (int t = 0; t < C::NUM_PE; ++t) sm100::mbar_init(&p_empty[t], 2 * C::NUM_DRAIN_WARPS);
     sm100::mbar_init(acc_empty, 2 * C::NUM_DRAIN_WARPS);
     sm100::fence_mbar_init();
   }
@@ -304,7 +314,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PsCfg<V, S>::NUM_THR
           const int o = g % C::NOP;
           sm100::mbar_wait(&op_full[o], (g / C::NOP) & 1);
           sm100::tc_fence_after();
-          if (kb == 0 && gtile > 0) {  // the previous tile's epilogue has read the accumulators
+          // the previous tile's epilogue has read the accumulators (kSchIn4RN: its
+          // epilogue reads registers only, the P buffers are guarded per block)
+          if (S != kSchIn4RN && kb == 0 && gtile > 0) {
             sm100::mbar_wait_cluster(acc_empty, (gtile - 1) & 1);
             sm100::tc_fence_after();
           }
@@ -318,6 +330,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PsCfg<V, S>::NUM_THR
             for (int ks = 0; ks < 4; ++ks)
               sm100::mma_pair_split<V == kTF32>(tmem_P, ahi + 2 * ks, hi_w, bhi + 2 * ks, hi_w, idesc,
                                                 (kb | ks) != 0);
+          } else if constexpr (S == kSchIn4RN) {
+            // per MMA k-step, the four terms in the reference's order, each into
+            // its own accumulator; a block's first k-step waits for the drain of
+            // that accumulator's previous block and starts it from zero
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {
+              const int kk = kb * 4 + ks;
+              const bool first = (kk % de) == 0;
+#pragma unroll
+              for (int t = 0; t < 4; ++t) {
+                if (first && git > 0) {
+                  sm100::mbar_wait_cluster(&p_empty[t], (git - 1) & 1);
+                  sm100::tc_fence_after();
+                }
+                sm100::mma_pair_split<V == kTF32>(tmem_P + t * C::BN, (t < 2 ? alo : ahi) + 2 * ks,
+                                                  hi_w, ((t & 1) ? bhi : blo) + 2 * ks, hi_w, idesc,
+                                                  !first);
+              }
+              if ((kk % de) == de - 1 || (kb == nop - 1 && ks == 3)) {
+                sm100::mma_commit_pair_mc(p_full, 0x3);
+                ++git;
+              }
+            }
           } else if constexpr (S == kSchIn4) {
             // the reference's four-call order per block: dA*dB, dA*B, A*dB, A*B
 #pragma unroll
@@ -351,7 +386,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PsCfg<V, S>::NUM_THR
                                                 !(first_in_interval && ks == 0));
           }
           sm100::mma_commit_pair_mc(&op_empty[o], 0x3);
-          if (kb == nop - 1 || (C::kDrain && (kb % de) == de - 1)) {
+          if (S != kSchIn4RN && (kb == nop - 1 || (C::kDrain && (kb % de) == de - 1))) {
             sm100::mma_commit_pair_mc(p_full, 0x3);
             ++git;
           }
@@ -391,6 +426,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PsCfg<V, S>::NUM_THR
           sm100::tc_fence_before();
           __syncwarp();
           if (lane == 0) sm100::mbar_arrive_remote(p_empty_leader);
+        } else if constexpr (S == kSchIn4RN) {
+          // mma.py:84-85 with an RN terminal, per term in order: c = RN32(c + P_t);
+          // each accumulator is released as soon as it has been read
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+#pragma unroll
+            for (int c = 0; c < NC / 8; ++c) {
+              uint32_t r[8];
+              sm100::tmem_ld_32x32b_x8(tmem_P + t * C::BN + lane_off + h * NC + c * 8, r);
+              sm100::tmem_ld_wait();
+#pragma unroll
+              for (int j = 0; j < 8; j += 2)
+                sm100::fadd2_rn(acc[c * 8 + j], acc[c * 8 + j + 1], __uint_as_float(r[j]),
+                                __uint_as_float(r[j + 1]));
+            }
+            sm100::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) sm100::mbar_arrive_remote(p_empty_leader + t * 8);
+          }
         }
       }
       // epilogue: every MMA of the tile has completed (its last p_full follows them)
@@ -400,8 +454,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PsCfg<V, S>::NUM_THR
 #pragma unroll
       for (int c = 0; c < NC / 8; ++c) {
         uint32_t r[8];
-        sm100::tmem_ld_32x32b_x8((C::kDrain ? tmem_dC : tmem_P) + lane_off + h * NC + c * 8, r);
-        sm100::tmem_ld_wait();
+        if constexpr (S != kSchIn4RN) {
+          sm100::tmem_ld_32x32b_x8((C::kDrain ? tmem_dC : tmem_P) + lane_off + h * NC + c * 8, r);
+          sm100::tmem_ld_wait();
+        }
         uint32_t rr[8];
         if constexpr (S == kSchC3DD) {
           sm100::tmem_ld_32x32b_x8(tmem_ddC + lane_off + h * NC + c * 8, rr);
@@ -415,6 +471,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PsCfg<V, S>::NUM_THR
             o[j] = __fmaf_rn(__uint_as_float(r[j]), inv_scale, acc[c * 8 + j]);
             if constexpr (S == kSchC3DD)  // schemes.py:312-313: then + ddC * 2^-2s
               o[j] = __fmaf_rn(__uint_as_float(rr[j]), inv_scale2, o[j]);
+          } else if constexpr (S == kSchIn4RN) {
+            o[j] = acc[c * 8 + j];
           } else {
             o[j] = __uint_as_float(r[j]);
           }

@@ -5,8 +5,10 @@ factories :87-123, SCHEMES_BY_NAME :126-137, RunFlags / GemmRun :140-153,
 default_config :156-160, gemm :317-373) for the path this package accelerates:
 the three-term corrected scheme (`corrected3`) with the scaled FP16 split
 (FP16-TCEC) or the TF32 split (TF32-TCEC).  The compute runs in the sm_100a
-kernel behind include/tcec.h; there is no CPU fallback.  Other scheme kinds
-(the reference's CPU comparators and ablations) raise NotImplementedError.
+kernel behind include/tcec.h; there is no CPU fallback.  The reference's
+in-unit comparators (tc_plain, markidis4, corrected4) run on the tensor core
+too (resolve_schedule); its CPU baselines (fp64_ref, fp32_simt,
+fp32_lsbtrunc) raise NotImplementedError.
 
 Error behaviour follows the reference: ValueError for non-2-D inputs,
 mismatched inner dimensions, non-finite inputs and non-FP32 values
@@ -158,17 +160,28 @@ STAGE_K = {N.TCEC_FP16: 64, N.TCEC_TF32: 32}
 DEFAULT_DRAIN_K = {N.TCEC_FP16: 128, N.TCEC_TF32: 64}
 
 
-def drain_k_for(variant: int, block_k: int) -> int:
+MMA_K = {N.TCEC_FP16: 16, N.TCEC_TF32: 8}
+
+
+def drain_k_for(variant: int, block_k: int, sched: int = 0) -> int:
     """Drain interval the kernel uses for MmaConfig.block_k: the reference's
     per-block drain (block_k = 16) is never more accurate on the hardware than
     the default interval, so block_k selects max(default, block_k rounded up to
-    whole operand stages)."""
+    whole operand stages).  corrected4_rn (SCHED_INUNIT4_RN) drains every block
+    of every product, so there block_k is taken as is (a multiple of the MMA
+    k-step)."""
+    if sched == SCHED_INUNIT4_RN:
+        if int(block_k) % MMA_K[variant]:
+            raise NotImplementedError(
+                f"corrected4_rn on the tensor core needs block_k a multiple of {MMA_K[variant]}")
+        return int(block_k)
     stage = STAGE_K[variant]
     return max(DEFAULT_DRAIN_K[variant], stage * max(1, -(-int(block_k) // stage)))
 
 
 # Product schedules of the kernel (include/tcec.h TCEC_SCHEME_*).
 SCHED_CORRECTED3, SCHED_CORRECTED3_DD, SCHED_TC_PLAIN, SCHED_INUNIT4 = 0, 1, 2, 3
+SCHED_INUNIT4_RN = 4
 
 
 def resolve_scheme(scheme) -> tuple[int, int, int]:
@@ -184,10 +197,10 @@ def resolve_scheme(scheme) -> tuple[int, int, int]:
 def resolve_schedule(scheme) -> tuple[int, int, int, int]:
     """(variant, rounding code, scale_log2, product schedule) of any scheme the
     tensor core can run: corrected3 (the accelerated path) and the reference's
-    in-unit comparators tc_plain (schemes.py:343-351) and markidis4 /
-    corrected4 with the RZ terminal (schemes.py:352-364) -- the hardware
-    accumulator's terminal rounding is fixed, so corrected4 with an RN
-    terminal is emulator-only.  fp64_ref / fp32_simt / fp32_lsbtrunc are the
+    in-unit comparators tc_plain (schemes.py:343-351), markidis4 / corrected4
+    with the RZ terminal (schemes.py:352-364, the hardware accumulator's own
+    rounding) and corrected4 with the RN terminal (each product's block drained
+    and added RN on the CUDA cores, SCHED_INUNIT4_RN).  fp64_ref / fp32_simt / fp32_lsbtrunc are the
     reference's CPU baselines and are not run here."""
     if isinstance(scheme, str):
         if scheme not in SCHEMES_BY_NAME:
@@ -206,14 +219,13 @@ def resolve_schedule(scheme) -> tuple[int, int, int, int]:
         raise NotImplementedError(f"tc_plain in {f!r} has no tensor-core kind here")
     if kind in (GemmKind.MARKIDIS4.value, GemmKind.CORRECTED4.value):
         term = getattr(getattr(scheme, "terminal", None), "value", "rz")
-        if kind == GemmKind.CORRECTED4.value and term != "rz":
-            raise NotImplementedError(
-                "corrected4 with an RN terminal is emulator-only: the tensor core's "
-                "accumulator rounding is fixed (run corrected4_rz / markidis4 on hardware)")
+        if kind == GemmKind.CORRECTED4.value and term not in ("rz", "rn"):
+            raise NotImplementedError(f"corrected4 with terminal {term!r} has no tensor-core form")
         variant, rounding, scale = native_split_args(scheme.split)
         if scale != 0:
             raise ValueError("in-unit four-term schemes require an unscaled split")
-        return variant, rounding, 0, SCHED_INUNIT4
+        rn = kind == GemmKind.CORRECTED4.value and term == "rn"
+        return variant, rounding, 0, SCHED_INUNIT4_RN if rn else SCHED_INUNIT4
     raise NotImplementedError(
         f"scheme kind {kind!r} is a CPU baseline of the reference; the sm_100a path runs "
         "corrected3 (FP16-TCEC / TF32-TCEC) and the in-unit tensor-core comparators")
@@ -297,7 +309,7 @@ def gemm_device(a, b, scheme="corrected3_halfhalf", cfg: MmaConfig | None = None
     if k == 0:  # zero blocks: C = 0 exactly (schemes.py:300-307)
         return out.zero_()
     block_k = cfg.block_k if cfg is not None else 16
-    dk = drain_k if drain_k is not None else drain_k_for(variant, block_k)
+    dk = drain_k if drain_k is not None else drain_k_for(variant, block_k, sched)
     opts = N.make_opts(split_rounding=rounding, scale_log2=scale,
                        drain_k=dk, block_n=block_n, group_m=group_m,
                        prefetch=prefetch, kernel_variant=kernel_variant,
@@ -398,7 +410,7 @@ def gemm(a, b, scheme, cfg: MmaConfig | None = None, out=None) -> GemmRun:
         C = np.empty((m, n), dtype=np.float32)
     fl = ctypes.c_uint32(0)
     opts = N.make_opts(split_rounding=rounding, scale_log2=scale,
-                       drain_k=drain_k_for(variant, block_k), scheme=sched)
+                       drain_k=drain_k_for(variant, block_k, sched), scheme=sched)
     N.check(N.lib().tcec_sgemm_host(variant, m, n, k, A.ctypes.data, max(k, 1), B.ctypes.data,
                                     max(n, 1), C.ctypes.data, max(n, 1), ctypes.byref(opts),
                                     ctypes.byref(fl), None), "tcec_sgemm_host")

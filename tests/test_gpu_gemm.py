@@ -301,8 +301,8 @@ def test_reference_scheme_objects_are_accepted():
     c4, _ = _run(a, b, T.corrected3(T.markidis_halfhalf()))
     oc, _ = O.corrected3(a, b, "fp16u", block_k=16, drain_k=128)
     _check_close(c4, oc, a, b, "fp16 unscaled", "fp16u")
-    # CPU baselines and the RN-terminal in-unit scheme have no tensor-core form
-    for name in ("corrected4_rn", "fp32_simt", "fp64_ref"):
+    # the CPU baselines have no tensor-core form
+    for name in ("fp32_simt", "fp64_ref", "fp32_lsbtrunc"):
         with pytest.raises(NotImplementedError):
             T.gemm(a, b, name)
 
@@ -440,11 +440,16 @@ def test_split_once_mode_flags_and_overflow(sname):
 # ----------------------------------------------------------------------------
 # In-unit comparator schemes on the tensor core
 
-INUNIT_HW = ["tc_plain_fp16", "tc_plain_tf32", "markidis4", "corrected4_rz", "markidis4_tf32"]
+INUNIT_HW = ["tc_plain_fp16", "tc_plain_tf32", "markidis4", "corrected4_rz", "markidis4_tf32",
+             "corrected4_rn"]
 
 
 def _inunit_scheme(T, name):
-    return T.markidis4(T.TF32) if name == "markidis4_tf32" else name
+    if name == "markidis4_tf32":
+        return T.markidis4(T.TF32)
+    if name == "corrected4_rn_tf32":
+        return T.corrected4(T.RoundingMode.RN, T.tf32tf32())
+    return name
 
 
 def _inunit_mag(a, b, name):
@@ -496,11 +501,15 @@ def test_inunit_accuracy_ordering_on_hardware():
     a = O.urand(64, 4096, -1, 1, 0)
     b = O.urand(4096, 64, -1, 1, O.pair_seed(0))
     ref = O.fp64_ref(a, b)
-    for name in ("corrected3_halfhalf", "markidis4", "tc_plain_fp16"):
+    for name in ("corrected3_halfhalf", "markidis4", "tc_plain_fp16", "corrected4_rn"):
         rel[name] = T.relative_residual(T.gemm(a, b, name).output, ref)
     rel["simt"] = T.relative_residual(O.fp32_simt(a, b), ref)
     assert rel["corrected3_halfhalf"] <= 2.0 * rel["simt"], rel
     assert rel["markidis4"] >= 4.0 * rel["corrected3_halfhalf"], rel
+    # the paper's point: the same four terms with an RN terminal (the CUDA-core
+    # add of each drained block) recover SGEMM accuracy -- RZ was the loss
+    assert rel["corrected4_rn"] <= 2.0 * rel["simt"], rel
+    assert rel["markidis4"] >= 4.0 * rel["corrected4_rn"], rel
     assert rel["tc_plain_fp16"] >= 100.0 * rel["corrected3_halfhalf"], rel
 
 
@@ -548,6 +557,56 @@ def test_inunit_ragged_vs_oracle(name, shape):
     mag, terms = _inunit_mag(a, b, name)
     bound = (terms * (-(-k // 16)) + 2) * 2.0 ** -22 * mag
     assert np.all(np.abs(run.output.astype(np.float64) - ref) <= bound)
+
+
+@pytest.mark.parametrize("name,block_k,shape", [
+    ("corrected4_rn", 16, (2048, 1536, 200)),     # 96 tiles: pairs walk two tiles
+    ("corrected4_rn", 32, (300, 200, 1000)),
+    ("corrected4_rn", 64, (129, 130, 777)),       # blocks span whole operand stages
+    ("corrected4_rn", 48, (64, 64, 200)),         # blocks straddle operand stages
+    ("corrected4_rn_tf32", 16, (300, 200, 1000)),
+    ("corrected4_rn_tf32", 8, (77, 513, 130)),
+])
+def test_corrected4_rn_blocks_vs_oracle(name, block_k, shape):
+    """corrected4 with the RN terminal (TCEC_SCHEME_INUNIT4_RN): every product's
+    block of block_k is drained and added RN in the reference's term order, so the
+    oracle at the same block_k is matched within the in-unit bound (the only
+    difference is the hardware's in-block accumulation); flags exact."""
+    T = _T()
+    m, n, k = shape
+    a = O.urand(m, k, -1, 1, 5 * m + k)
+    b = O.urand(k, n, -1, 1, 7 * n + k)
+    scheme = _inunit_scheme(T, name)
+    sch = T.SCHEMES_BY_NAME[scheme] if isinstance(scheme, str) else scheme
+    run = T.gemm(a, b, scheme, T.default_config(sch, block_k=block_k))
+    if m * n > 100_000:  # the oracle on a sub-block (rows / columns are separable)
+        rows = np.r_[0:8, m // 2:m // 2 + 8, m - 8:m]
+        cols = np.r_[0:16, n - 16:n]
+        ref, fl = O.inunit(a[rows], b[:, cols], name, block_k=block_k)
+        got = run.output[np.ix_(rows, cols)]
+        mag, terms = _inunit_mag(a[rows], b[:, cols], name)
+    else:
+        ref, fl = O.inunit(a, b, name, block_k=block_k)
+        got = run.output
+        mag, terms = _inunit_mag(a, b, name)
+        assert (run.flags.saw_overflow, run.flags.saw_out_of_range) == (bool(fl & 1), bool(fl & 2))
+    bound = (terms * (-(-k // block_k)) + 2) * 2.0 ** -22 * mag
+    diff = np.abs(got.astype(np.float64) - ref)
+    assert np.all(diff <= bound), float(np.max(diff / bound))
+    # the RN terminal's error does not grow like the RZ one: against FP64 the
+    # result is within SGEMM's accuracy
+    sim = O.fp32_simt(a[:64], b)
+    f64 = O.fp64_ref(a[:64], b)
+    assert T.relative_residual(run.output[:64], f64) <= 2.0 * T.relative_residual(sim, f64)
+
+
+def test_corrected4_rn_rejects_partial_k_step():
+    """block_k must be a whole number of MMA k-steps (16 FP16 / 8 TF32)."""
+    T = _T()
+    a = O.urand(32, 64, -1, 1, 1)
+    b = O.urand(64, 32, -1, 1, 2)
+    with pytest.raises(NotImplementedError):
+        T.gemm(a, b, "corrected4_rn", T.default_config(T.SCHEMES_BY_NAME["corrected4_rn"], block_k=24))
 
 
 @pytest.mark.parametrize("sname,variant,bk,drain", VARIANTS)
