@@ -77,7 +77,8 @@ typedef struct tcec_opts {
    * multiple of the operand stage depth (64 for FP16, 32 for TF32).
    * TCEC_SCHEME_INUNIT4_RN: the block of each drained product (see above). */
   int32_t drain_k;
-  /* Output tile width: 0 = default (256: CTA-pair 256 x 256 tile); 128 = single-CTA 128 x 128;
+  /* Output tile width: 0 = automatic (the CTA-pair 256 x 256 tile, or 256 x 192
+   * when that tiling fits one wave of CTA pairs; same results); 128 = single-CTA 128 x 128;
    * 192 = CTA-pair 256 x 192 tile with the split A operand in tensor memory. */
   int32_t block_n;
   /* Tile rasterisation group along m in 128-row tiles: 0 = default (8). */

@@ -533,8 +533,9 @@ int sgemm_impl(int variant, int64_t m, int64_t n, int64_t k, const float* A, int
     if (o.drain_k < 0 || o.drain_k % bk_op != 0) return TCEC_ERR_UNSUPPORTED;
     drain_every = o.drain_k / bk_op;
   }
-  const int block_n = o.block_n == 0 ? 256 : o.block_n;
-  if (block_n != 128 && block_n != 192 && block_n != 256) return TCEC_ERR_UNSUPPORTED;
+  int block_n = o.block_n;
+  if (block_n != 0 && block_n != 128 && block_n != 192 && block_n != 256)
+    return TCEC_ERR_UNSUPPORTED;
   const int group_m = o.group_m <= 0 ? 8 : o.group_m;
   // reserved[0]: L2 prefetch distance in 32-deep k-slices (pair kernel; 0 = off)
   const int prefetch = o.reserved[0] < 0 ? 0 : (o.reserved[0] > 16 ? 16 : o.reserved[0]);
@@ -552,6 +553,20 @@ int sgemm_impl(int variant, int64_t m, int64_t n, int64_t k, const float* A, int
   const int scheme = o.scheme;
   if (scheme < TCEC_SCHEME_CORRECTED3 || scheme > TCEC_SCHEME_INUNIT4_RN) return TCEC_ERR_UNSUPPORTED;
   if (in_unit && o.scale_log2 > 0) return TCEC_ERR_UNSUPPORTED;
+  if (block_n == 0) {
+    // automatic tile: 256 x 192 when that tiling still fits one wave of CTA
+    // pairs, so a small product keeps more SMs busy than the 256 x 256 tiling
+    // (measured +12-18% at 1024^2 and 1536^2, profiles/r01/smallbn.log); else
+    // 256 x 256.  Results are bit-identical either way.
+    block_n = 256;
+    if (kvariant == 0 && mma_order == 0 && prefetch == 0 && split_mode != 2 &&
+        scheme == TCEC_SCHEME_CORRECTED3 && ex == nullptr) {
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      if (((m + 255) / 256) * ((n + 191) / 192) <= sms / 2) block_n = 192;
+    }
+  }
   if (m == 0 || n == 0) return TCEC_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (k == 0) {
