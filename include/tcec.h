@@ -98,7 +98,8 @@ typedef struct tcec_opts {
   /* reserved[0]: L2 prefetch distance in 32-deep k-slices (0 = off);
    * reserved[1]: pair-kernel variant (0 = automatic: persistent with lock-step waves for
    *              products of >= 8 waves of tiles, else per-tile; 1 = unified split/drain
-   *              workers; 2 = persistent; 3 = persistent, lock-step waves; 4 = per-tile);
+   *              workers; 2 = persistent; 3 = persistent, lock-step waves; 4 = per-tile;
+   *              5 = persistent clusters of two pairs sharing the split of A -- slower);
    * reserved[2]: pair-kernel MMA order (0 = corrections first, 1 = A_hi collector reuse). */
   int32_t reserved[3];
 } tcec_opts;

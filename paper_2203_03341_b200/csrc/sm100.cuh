@@ -254,6 +254,20 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
                : "memory");
 }
 
+// 16-byte store into another CTA's shared memory (shared::cluster address).
+__device__ __forceinline__ void sts128_cluster(uint32_t cluster_addr, uint32_t a, uint32_t b,
+                                               uint32_t c, uint32_t d) {
+  asm volatile("st.shared::cluster.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(cluster_addr), "r"(a),
+               "r"(b), "r"(c), "r"(d)
+               : "memory");
+}
+
+// Order this thread's generic-proxy shared-memory writes (local and in peer
+// CTAs) before later async-proxy (tensor core) reads of them.
+__device__ __forceinline__ void fence_proxy_async_cluster() {
+  asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");
+}
+
 // Arrive on an mbarrier in another CTA of the cluster with the default
 // (CTA-scope release) semantics -- no GPU-scope fence.  Used where the arrive
 // only has to order this thread's completed TMEM reads, not memory writes.

@@ -6,6 +6,7 @@
 // from the runtime (no link-time libcuda dependency).
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -19,6 +20,7 @@
 #include "tcec_gemm3.cuh"
 #include "tcec_gemm4.cuh"
 #include "tcec_gemm5.cuh"
+#include "tcec_gemm6.cuh"
 #include "tcec_presplit.cuh"
 #include "tcec_census.cuh"
 
@@ -380,6 +382,77 @@ int launch_gemm_pers(int64_t m, int64_t n, int64_t k, const float* A, int64_t ld
   return launched ? TCEC_OK : TCEC_ERR_CUDA;
 }
 
+// Persistent CTA-quad kernel (kernel_variant 5): two pairs per cluster of four
+// share the split of A (tcec_gemm6.cuh).  The grid is the number of co-resident
+// clusters of four (GPCs with an odd number of TPCs leave one idle).
+template <int V, int R>
+int launch_gemm_quad(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, const float* B,
+                     int64_t ldb, float* C, int64_t ldc, int scale_log2, int drain_every,
+                     int group_m, bool lockstep_ok, uint32_t* d_flags, cudaStream_t stream) {
+  using Cfg = tcec::QuadCfg<V>;
+  using VC = tcec::VarCfg<V>;
+  CUtensorMap tmA, tmB;
+  int st;
+  if ((st = make_tmap(&tmA, A, k, m, lda, Cfg::BK_STG, Cfg::A_ROWS, CU_TENSOR_MAP_SWIZZLE_128B)))
+    return st;
+  if ((st = make_tmap(&tmB, B, n, k, ldb, 32, Cfg::BK_STG, CU_TENSOR_MAP_SWIZZLE_128B))) return st;
+  auto kern = tcec::tcec_gemm_quad_kernel<V, R>;
+  static std::once_flag attr_once;
+  static cudaError_t attr_err = cudaSuccess;
+  static int max_quads = 0;
+  std::call_once(attr_once, [&] {
+    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    Cfg::SMEM_BYTES);
+    if (attr_err != cudaSuccess) return;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(4, 1, 1);
+    cfg.blockDim = dim3(Cfg::NUM_THREADS, 1, 1);
+    cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+    if (cudaOccupancyMaxActiveClusters(&max_quads, kern, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      max_quads = 0;
+    }
+  });
+  if (attr_err != cudaSuccess) return TCEC_ERR_CUDA;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  tcec::GemmShape shp;
+  shp.m = static_cast<int32_t>(m);
+  shp.n = static_cast<int32_t>(n);
+  shp.k = static_cast<int32_t>(k);
+  shp.num_op_stages = static_cast<int32_t>((k + VC::BK_OP - 1) / VC::BK_OP);
+  shp.drain_every = drain_every;
+  shp.group_m = group_m;
+  shp.prefetch = 0;
+  shp.mma_order = 0;
+  const float scale = ldexpf(1.0f, scale_log2);
+  const float inv_scale = ldexpf(1.0f, -scale_log2);
+  const tcec::FlagThresholds thr = tcec::flag_thresholds(V, R, scale_log2);
+  const int64_t tiles_n = (n + Cfg::BN - 1) / Cfg::BN;
+  const int64_t units = ((m + 2 * Cfg::BM - 1) / (2 * Cfg::BM)) * ((tiles_n + 1) / 2);
+  int64_t quads = max_quads > 0 ? max_quads : sms / 4 - 4;
+  if (quads > units) quads = units;
+  if (quads < 1) quads = 1;
+  const bool lockstep = lockstep_ok && units >= 8 * quads;
+  uint32_t* wave_ctr = nullptr;
+  if (lockstep) {
+    keep_pool(dev);
+    if (cudaMallocAsync(reinterpret_cast<void**>(&wave_ctr), sizeof(uint32_t), stream) != cudaSuccess)
+      return TCEC_ERR_CUDA;
+    if (cudaMemsetAsync(wave_ctr, 0, sizeof(uint32_t), stream) != cudaSuccess) {
+      cudaFreeAsync(wave_ctr, stream);
+      return TCEC_ERR_CUDA;
+    }
+  }
+  kern<<<static_cast<unsigned>(4 * quads), Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream>>>(
+      tmA, tmB, C, ldc, shp, scale, inv_scale, thr, d_flags, wave_ctr);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  const bool launched = cudaGetLastError() == cudaSuccess;
+  if (wave_ctr) cudaFreeAsync(wave_ctr, stream);
+  return launched ? TCEC_OK : TCEC_ERR_CUDA;
+}
+
 template <int V, int R>
 int dispatch_bn(int bn, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda,
                 const float* B, int64_t ldb, float* C, int64_t ldc, int s, int de, int gm, int pf,
@@ -425,6 +498,11 @@ int dispatch_bn(int bn, int64_t m, int64_t n, int64_t k, const float* A, int64_t
         if (ex && ex->count > 0) return TCEC_ERR_UNSUPPORTED;
         const int g = gm_user > 0 ? (gm / 2 > 0 ? gm / 2 : 1) : (kv == 3 ? 8 : 4);
         return launch_gemm_pers<V, R>(m, n, k, A, lda, B, ldb, C, ldc, s, de, g, kv == 3, fl, st);
+      }
+      if (kv == 5) {  // persistent CTA quads sharing the A split
+        if (ex && ex->count > 0) return TCEC_ERR_UNSUPPORTED;
+        const int g = gm_user > 0 ? (gm / 2 > 0 ? gm / 2 : 1) : 8;
+        return launch_gemm_quad<V, R>(m, n, k, A, lda, B, ldb, C, ldc, s, de, g, true, fl, st);
       }
       if (kv == 4) kv = 0;  // the per-tile pair kernel
       if (kv == 1)
@@ -542,7 +620,7 @@ int sgemm_impl(int variant, int64_t m, int64_t n, int64_t k, const float* A, int
   // reserved[1]: pair-kernel variant (0 = automatic, 1 = unified split/drain workers,
   // 2 = persistent, 3 = persistent with lock-step waves, 4 = per-tile)
   const int kvariant = o.reserved[1];
-  if (kvariant < 0 || kvariant > 4) return TCEC_ERR_UNSUPPORTED;
+  if (kvariant < 0 || kvariant > 5) return TCEC_ERR_UNSUPPORTED;
   // reserved[2]: pair-kernel MMA order (0 = corrections then main term, 1 = A_hi collector reuse)
   const int mma_order = o.reserved[2];
   if (mma_order != 0 && mma_order != 1) return TCEC_ERR_UNSUPPORTED;
