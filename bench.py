@@ -140,6 +140,66 @@ class ClockSampler:
                 "power_w_max": max(power) if power else None, "reasons": sorted(reasons)}
 
 
+class NvmlClockSampler:
+    """The same record from NVML, polled every 10 ms on a background thread
+    (nvidia-smi's process start-up can leave a ~0.3 s timed region with one
+    sample).  Falls back to ClockSampler when NVML is unavailable."""
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.samples = []
+        self.thread = None
+        self.stop_evt = None
+        self.fallback = None
+
+    def start(self):
+        import threading
+
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            max_sm = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.fallback = ClockSampler(self.gpu)
+            self.fallback.start()
+            return
+        bits = {"hw_slowdown": pynvml.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
+        self.stop_evt = threading.Event()
+
+        def run():
+            while not self.stop_evt.is_set():
+                try:
+                    t = time.time()
+                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    pw = pynvml.nvmlDeviceGetPowerUsage(h) / 1000.0
+                    rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.samples.append((t, sm, max_sm, pw, [n for n, b in bits.items() if rs & b]))
+                except Exception:
+                    pass
+                self.stop_evt.wait(0.01)
+
+        self.thread = threading.Thread(target=run, daemon=True)
+        self.thread.start()
+
+    def stop(self, window=None):
+        if self.fallback is not None:
+            return self.fallback.stop(window)
+        self.stop_evt.set()
+        self.thread.join(timeout=2)
+        rows = [r for r in self.samples if window is None or window[0] <= r[0] <= window[1]]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        reasons = sorted({n for r in rows for n in r[4]})
+        return {"sm_mhz": statistics.median(r[1] for r in rows), "sm_max_mhz": max(r[2] for r in rows),
+                "samples": len(rows), "power_w_max": max(r[3] for r in rows), "reasons": reasons,
+                "source": "nvml, 10 ms"}
+
+
 # ------------------------------------------------------------ CPU oracle ---
 def cpu_oracle_sample(variant: str, k: int, seconds: float, threads: int, rows: int | None = None):
     """Time the CPU oracle (test-infrastructure restatement of the reference's
@@ -262,7 +322,7 @@ def main():
     for _ in range(args.warmup):
         step()
     barrier()
-    clocks = ClockSampler(local)
+    clocks = NvmlClockSampler(local)
     clocks.start()
     time.sleep(0.3)
     launches0 = Nat.launch_count()
