@@ -9,6 +9,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <set>
+#include <utility>
 
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -108,6 +110,24 @@ struct ExtraC {
   int count;
 };
 
+// Dynamic shared-memory opt-in, once per (kernel, device): the attribute
+// belongs to the device context, so a process driving several GPUs sets it on
+// each of them.
+template <typename K>
+cudaError_t smem_optin(K kern, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const auto key = std::make_pair(reinterpret_cast<const void*>(kern), dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count(key)) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.insert(key);
+  return e;
+}
+
 template <int V, int R, int BN>
 int launch_gemm(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, const float* B,
                 int64_t ldb, float* C, int64_t ldc, int scale_log2, int drain_every, int group_m,
@@ -123,12 +143,7 @@ int launch_gemm(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, co
     return st;
 
   auto kern = tcec::tcec_gemm_kernel<V, R, BN>;
-  static std::once_flag attr_once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(attr_once, [&] {
-    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    Cfg::SMEM_BYTES);
-  });
+  const cudaError_t attr_err = smem_optin(kern, Cfg::SMEM_BYTES);
   if (attr_err != cudaSuccess) return TCEC_ERR_CUDA;
 
   tcec::GemmShape shp;
@@ -171,12 +186,7 @@ int launch_gemm_pair(int64_t m, int64_t n, int64_t k, const float* A, int64_t ld
       return st;
 
   auto kern = kUnified ? tcec::tcec_gemm_pair_uni_kernel<V, R> : tcec::tcec_gemm_pair_kernel<V, R>;
-  static std::once_flag attr_once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(attr_once, [&] {
-    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    Cfg::SMEM_BYTES);
-  });
+  const cudaError_t attr_err = smem_optin(kern, Cfg::SMEM_BYTES);
   if (attr_err != cudaSuccess) return TCEC_ERR_CUDA;
 
   tcec::GemmShape shp;
@@ -212,12 +222,7 @@ int launch_gemm_ts(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda,
   if ((st = make_tmap(&tmC, C, n, m, ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B))) return st;
 
   auto kern = tcec::tcec_gemm_ts_kernel<V, R, BN, NOP>;
-  static std::once_flag attr_once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(attr_once, [&] {
-    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    Cfg::SMEM_BYTES);
-  });
+  const cudaError_t attr_err = smem_optin(kern, Cfg::SMEM_BYTES);
   if (attr_err != cudaSuccess) return TCEC_ERR_CUDA;
 
   tcec::GemmShape shp;
@@ -270,12 +275,7 @@ int launch_gemm_presplit(int64_t m, int64_t n, int64_t k, const float* A, int64_
   if (!st) st = make_tmap_op(&tmBh, bh, dt, esize, k, n, ldk, Cfg::BN_CTA);
   if (!st) st = make_tmap_op(&tmBl, bl, dt, esize, k, n, ldk, Cfg::BN_CTA);
   auto kern = tcec::tcec_gemm_ps_kernel<V, S>;
-  static std::once_flag attr_once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(attr_once, [&] {
-    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    Cfg::SMEM_BYTES);
-  });
+  const cudaError_t attr_err = smem_optin(kern, Cfg::SMEM_BYTES);
   if (!st && attr_err != cudaSuccess) st = TCEC_ERR_CUDA;
   // persistent: one pair per TPC; lock-step waves of 8 x 9 tiles from 8 waves on
   int sms = 148;
@@ -338,12 +338,7 @@ int launch_gemm_pers(int64_t m, int64_t n, int64_t k, const float* A, int64_t ld
     return st;
   if ((st = make_tmap(&tmB, B, n, k, ldb, 32, Cfg::BK_STG, CU_TENSOR_MAP_SWIZZLE_128B))) return st;
   auto kern = tcec::tcec_gemm_pers_kernel<V, R>;
-  static std::once_flag attr_once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(attr_once, [&] {
-    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    Cfg::SMEM_BYTES);
-  });
+  const cudaError_t attr_err = smem_optin(kern, Cfg::SMEM_BYTES);
   if (attr_err != cudaSuccess) return TCEC_ERR_CUDA;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -397,22 +392,27 @@ int launch_gemm_quad(int64_t m, int64_t n, int64_t k, const float* A, int64_t ld
     return st;
   if ((st = make_tmap(&tmB, B, n, k, ldb, 32, Cfg::BK_STG, CU_TENSOR_MAP_SWIZZLE_128B))) return st;
   auto kern = tcec::tcec_gemm_quad_kernel<V, R>;
-  static std::once_flag attr_once;
-  static cudaError_t attr_err = cudaSuccess;
-  static int max_quads = 0;
-  std::call_once(attr_once, [&] {
-    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    Cfg::SMEM_BYTES);
-    if (attr_err != cudaSuccess) return;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(4, 1, 1);
-    cfg.blockDim = dim3(Cfg::NUM_THREADS, 1, 1);
-    cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
-    if (cudaOccupancyMaxActiveClusters(&max_quads, kern, &cfg) != cudaSuccess) {
-      cudaGetLastError();
-      max_quads = 0;
+  const cudaError_t attr_err = smem_optin(kern, Cfg::SMEM_BYTES);
+  // co-resident clusters of four, per device
+  static std::mutex occ_mu;
+  static int occ_quads[64] = {0};
+  int max_quads = 0;
+  if (attr_err == cudaSuccess) {
+    int d = 0;
+    cudaGetDevice(&d);
+    std::lock_guard<std::mutex> lk(occ_mu);
+    if (d >= 0 && d < 64 && occ_quads[d] == 0) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(4, 1, 1);
+      cfg.blockDim = dim3(Cfg::NUM_THREADS, 1, 1);
+      cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+      if (cudaOccupancyMaxActiveClusters(&occ_quads[d], kern, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        occ_quads[d] = -1;
+      }
     }
-  });
+    if (d >= 0 && d < 64) max_quads = occ_quads[d];
+  }
   if (attr_err != cudaSuccess) return TCEC_ERR_CUDA;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
