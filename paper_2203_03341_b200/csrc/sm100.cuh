@@ -254,6 +254,14 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
                : "memory");
 }
 
+// Named barrier over `kThreads` threads (warp multiples) of this CTA; the
+// non-.aligned form, so lanes that left a lane-0 branch need not reconverge.
+template <uint32_t kId, uint32_t kThreads>
+__device__ __forceinline__ void named_barrier_sync() {
+  __syncwarp();
+  asm volatile("barrier.sync %0, %1;" ::"n"(kId), "n"(kThreads) : "memory");
+}
+
 // 16-byte store into another CTA's shared memory (shared::cluster address).
 __device__ __forceinline__ void sts128_cluster(uint32_t cluster_addr, uint32_t a, uint32_t b,
                                                uint32_t c, uint32_t d) {

@@ -324,6 +324,8 @@ __global__ void __launch_bounds__(TileCfg<BN>::NUM_THREADS, 1)
       if (lane == 0) sm100::mbar_arrive(&op_full[o]);
     }
     flag_publish(fa, thr, flags);
+    // the epilogue reuses the staging ring (see the drain warps' barrier)
+    sm100::named_barrier_sync<1, 32 * (C::NUM_SPLIT_WARPS + C::NUM_DRAIN_WARPS)>();
   } else if (warp >= C::DRAIN_WARP0) {
     // ===================== drain + epilogue warps =====================
     constexpr int HALF = BN / 2;
@@ -349,7 +351,10 @@ __global__ void __launch_bounds__(TileCfg<BN>::NUM_THREADS, 1)
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(p_empty);
     }
-    // Epilogue: every MMA has completed (the last p_full commit follows them).
+    // Epilogue: every MMA has completed (the last p_full commit follows them), and
+    // with it every split warp's staging read; the named barrier states it for
+    // tools that do not follow mbarrier / tcgen05.commit ordering (racecheck)
+    sm100::named_barrier_sync<1, 32 * (C::NUM_SPLIT_WARPS + C::NUM_DRAIN_WARPS)>();
     bool nonfinite = false;
     uint8_t* stage = smem + C::OFF_STG + (warp - C::DRAIN_WARP0) * (HALF / C::EPI_BOX) * 4096;
 #pragma unroll

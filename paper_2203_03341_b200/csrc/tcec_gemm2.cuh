@@ -441,6 +441,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
     } else {
       pair_split_loop<V, R, false>(smem_base, stg_full, stg_empty, op_full, op_empty, nop, t, lane, scale, fa);
     }
+    // the epilogue reuses the staging ring: see the drain warps' barrier below
+    sm100::named_barrier_sync<1, 32 * (C::NUM_SPLIT_WARPS + C::NUM_DRAIN_WARPS)>();
   } else {
     // setmaxnreg can only redistribute the launch allocation (96 x 640 registers):
     // 4 x 40 + 8 x 56 + 8 x 160 = 1888 <= 20 x 96 = 1920 per lane slot
@@ -472,7 +474,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
       // the TMEM reads above have completed (wait::ld); P may be overwritten
       if (lane == 0) sm100::mbar_arrive_remote(p_empty_leader);
     }
-    // every MMA of the pair has completed (the last p_full commit follows them)
+    // every MMA of the pair has completed (the last p_full commit follows them),
+    // and so have this CTA's split warps' staging reads; the named barrier says
+    // so explicitly (racecheck does not follow mbarrier / tcgen05.commit chains)
+    sm100::named_barrier_sync<1, 32 * (C::NUM_SPLIT_WARPS + C::NUM_DRAIN_WARPS)>();
     bool nonfinite = false;
     const uint32_t stage = smem_base + (warp - C::DRAIN_WARP0) * C::EPI_WARP_BYTES;
 #pragma unroll

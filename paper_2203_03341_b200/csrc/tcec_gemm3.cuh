@@ -304,7 +304,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(UniCfg::NUM_THREADS,
       uni_worker_loop<V, R, false>(smem_base, stg_full, stg_empty, op_full, op_empty, p_full,
                                    p_empty, tmem_P, nop, de, t, lane, scale, fa, acc);
     }
-    // every MMA of the pair has completed (the last p_full follows them)
+    // every MMA of the pair has completed (the last p_full follows them); all
+    // workers' staging reads precede the epilogue's staging writes
+    sm100::named_barrier_sync<1, 32 * U::NUM_WORKER_WARPS>();
     const int q = w & 3, cb = w >> 2;
     const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
     bool nonfinite = false;

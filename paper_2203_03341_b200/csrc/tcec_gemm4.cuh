@@ -327,6 +327,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
       ts_split_loop<V, R, false, BN, NOP>(smem_base, tmem_base, stg_full, stg_empty, op_full, op_empty, nop, t,
                                  lane, scale, fa);
     }
+    // the epilogue reuses the staging ring (see the drain warps' barrier)
+    sm100::named_barrier_sync<1, 32 * (C::NUM_SPLIT_WARPS + C::NUM_DRAIN_WARPS)>();
   } else {
     sm100::regs_inc<160>();
     // ===================== drain + epilogue =====================
@@ -355,6 +357,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
       if (lane == 0) sm100::mbar_arrive_remote(p_empty_leader);
     }
     bool nonfinite = false;
+    // the split warps' staging reads precede the epilogue's staging writes
+    sm100::named_barrier_sync<1, 32 * (C::NUM_SPLIT_WARPS + C::NUM_DRAIN_WARPS)>();
     const uint32_t stage = smem_base + (warp - C::DRAIN_WARP0) * C::EPI_WARP_BYTES;
 #pragma unroll
     for (int b = 0; b < NC / 32; ++b) {
