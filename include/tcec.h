@@ -95,6 +95,14 @@ typedef struct tcec_opts {
    * buffers are streamed in (0 = automatic, at most 8 each). */
   int32_t host_row_blocks;
   int32_t host_col_blocks;
+  /* Split-K parts (corrected3, fused split): 0 / 1 = off.  S > 1 splits k into
+   * S contiguous parts computed as separate persistent-kernel units; each part
+   * keeps its own main-term sum and dC, and a second kernel combines them in
+   * part order, C = RN(sum c_p + (sum dC_p) 2^-s) -- deterministic, but not the
+   * single-pass rounding sequence, so results match the reference within the
+   * GEMM tolerance instead of bit for bit.  For products with fewer output
+   * tiles than SMs (small m x n, long k). */
+  int32_t split_k;
   /* reserved[0]: L2 prefetch distance in 32-deep k-slices (0 = off);
    * reserved[1]: pair-kernel variant (0 = automatic: persistent with lock-step waves for
    *              products of >= 8 waves of tiles, else per-tile; 1 = unified split/drain

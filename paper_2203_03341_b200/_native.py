@@ -46,6 +46,7 @@ class TcecOpts(ctypes.Structure):
         ("scheme", ctypes.c_int32),
         ("host_row_blocks", ctypes.c_int32),
         ("host_col_blocks", ctypes.c_int32),
+        ("split_k", ctypes.c_int32),
         ("reserved", ctypes.c_int32 * 3),
     ]
 
@@ -110,8 +111,9 @@ def check(status: int, what: str) -> None:
 def make_opts(split_rounding: int = ROUND_DEFAULT, scale_log2: int = -1, drain_k: int = 0,
               block_n: int = 0, group_m: int = 0, prefetch: int = 0,
               kernel_variant: int = 0, mma_order: int = 0, split_mode: int = 0,
-              scheme: int = 0, host_blocks: tuple = (0, 0)) -> TcecOpts:
+              scheme: int = 0, host_blocks: tuple = (0, 0), split_k: int = 0) -> TcecOpts:
     o = TcecOpts()
+    o.split_k = split_k
     o.host_row_blocks, o.host_col_blocks = host_blocks
     o.split_mode = split_mode
     o.scheme = scheme

@@ -329,7 +329,8 @@ int launch_gemm_presplit(int64_t m, int64_t n, int64_t k, const float* A, int64_
 template <int V, int R>
 int launch_gemm_pers(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, const float* B,
                      int64_t ldb, float* C, int64_t ldc, int scale_log2, int drain_every,
-                     int group_m, bool lockstep, uint32_t* d_flags, cudaStream_t stream) {
+                     int group_m, bool lockstep, uint32_t* d_flags, cudaStream_t stream,
+                     int ksplit = 1) {
   using Cfg = tcec::PairCfg<V>;
   using VC = tcec::VarCfg<V>;
   CUtensorMap tmA, tmB;
@@ -355,7 +356,9 @@ int launch_gemm_pers(int64_t m, int64_t n, int64_t k, const float* A, int64_t ld
   const float scale = ldexpf(1.0f, scale_log2);
   const float inv_scale = ldexpf(1.0f, -scale_log2);
   const tcec::FlagThresholds thr = tcec::flag_thresholds(V, R, scale_log2);
-  const int64_t tiles = ((m + 2 * Cfg::BM - 1) / (2 * Cfg::BM)) * ((n + Cfg::BN - 1) / Cfg::BN);
+  if (ksplit > shp.num_op_stages) ksplit = shp.num_op_stages;
+  const int64_t tiles = ((m + 2 * Cfg::BM - 1) / (2 * Cfg::BM)) * ((n + Cfg::BN - 1) / Cfg::BN) *
+                        (ksplit > 1 ? ksplit : 1);
   int64_t pairs = sms / 2;
   if (pairs > tiles) pairs = tiles;
   if (pairs < 1) pairs = 1;
@@ -369,8 +372,37 @@ int launch_gemm_pers(int64_t m, int64_t n, int64_t k, const float* A, int64_t ld
       return TCEC_ERR_CUDA;
     }
   }
+  if (ksplit > 1) {
+    // split-K: (tile, part) units, partial sums to a stream-ordered workspace,
+    // then the fixed-order combine (tcec_splitk_reduce_kernel)
+    auto kern_sk = tcec::tcec_gemm_pers_kernel<V, R, true>;
+    if (smem_optin(kern_sk, Cfg::SMEM_BYTES) != cudaSuccess) {
+      if (wave_ctr) cudaFreeAsync(wave_ctr, stream);
+      return TCEC_ERR_CUDA;
+    }
+    const int64_t n8 = (n + 7) & ~int64_t(7);
+    float* ws = nullptr;
+    if (cudaMallocAsync(reinterpret_cast<void**>(&ws), sizeof(float) * 2 * ksplit * m * n8,
+                        stream) != cudaSuccess) {
+      if (wave_ctr) cudaFreeAsync(wave_ctr, stream);
+      return TCEC_ERR_CUDA;
+    }
+    kern_sk<<<static_cast<unsigned>(2 * pairs), Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream>>>(
+        tmA, tmB, C, ldc, shp, scale, inv_scale, thr, d_flags, wave_ctr, ws, ksplit);
+    bool ok = cudaGetLastError() == cudaSuccess;
+    const int64_t quads = m * (n8 / 4);
+    int64_t blocks = (quads + 255) / 256;
+    if (blocks > 8 * int64_t(sms)) blocks = 8 * int64_t(sms);
+    tcec::tcec_splitk_reduce_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
+        ws, ksplit, static_cast<int>(m), static_cast<int>(n), C, ldc, inv_scale, d_flags);
+    ok = ok && cudaGetLastError() == cudaSuccess;
+    g_launches.fetch_add(2, std::memory_order_relaxed);
+    cudaFreeAsync(ws, stream);
+    if (wave_ctr) cudaFreeAsync(wave_ctr, stream);
+    return ok ? TCEC_OK : TCEC_ERR_CUDA;
+  }
   kern<<<static_cast<unsigned>(2 * pairs), Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream>>>(
-      tmA, tmB, C, ldc, shp, scale, inv_scale, thr, d_flags, wave_ctr);
+      tmA, tmB, C, ldc, shp, scale, inv_scale, thr, d_flags, wave_ctr, nullptr, 1);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   const bool launched = cudaGetLastError() == cudaSuccess;
   if (wave_ctr) cudaFreeAsync(wave_ctr, stream);
@@ -457,9 +489,18 @@ template <int V, int R>
 int dispatch_bn(int bn, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda,
                 const float* B, int64_t ldb, float* C, int64_t ldc, int s, int de, int gm, int pf,
                 int kv, int mo, int sm, int sch, const ExtraC* ex, uint32_t* fl,
-                cudaStream_t st, int gm_user) {
+                cudaStream_t st, int gm_user, int sk = 0) {
   if (ex && ex->count > 0 && (bn != 256 || sm == 2 || sch != TCEC_SCHEME_CORRECTED3))
     return TCEC_ERR_UNSUPPORTED;  // extra destinations: the default pair kernels only
+  if (sk > 1) {  // split-K: the persistent pair kernel over (tile, part) units
+    if (sm == 2 || sch != TCEC_SCHEME_CORRECTED3 || (ex && ex->count > 0) || mo != 0 ||
+        (bn != 256 && bn != 0))
+      return TCEC_ERR_UNSUPPORTED;
+    const int g = gm_user > 0 ? (gm / 2 > 0 ? gm / 2 : 1) : 8;
+    // lock-step waves unless the caller pinned the per-tile variant (the host
+    // path's concurrent blocks)
+    return launch_gemm_pers<V, R>(m, n, k, A, lda, B, ldb, C, ldc, s, de, g, kv != 4, fl, st, sk);
+  }
   if (sm == 2 || sch != TCEC_SCHEME_CORRECTED3) {
     if ((bn != 256 && bn != 0) || (kv != 0 && kv != 4) || mo != 0) return TCEC_ERR_UNSUPPORTED;
     const int g = gm / 2 > 0 ? gm / 2 : 1;
@@ -631,6 +672,7 @@ int sgemm_impl(int variant, int64_t m, int64_t n, int64_t k, const float* A, int
   const int scheme = o.scheme;
   if (scheme < TCEC_SCHEME_CORRECTED3 || scheme > TCEC_SCHEME_INUNIT4_RN) return TCEC_ERR_UNSUPPORTED;
   if (in_unit && o.scale_log2 > 0) return TCEC_ERR_UNSUPPORTED;
+  if (o.split_k < 0 || o.split_k > 64) return TCEC_ERR_UNSUPPORTED;
   if (block_n == 0) {
     // automatic tile: 256 x 192 when that tiling still fits one wave of CTA
     // pairs, so a small product keeps more SMs busy than the 256 x 256 tiling
@@ -638,7 +680,7 @@ int sgemm_impl(int variant, int64_t m, int64_t n, int64_t k, const float* A, int
     // 256 x 256.  Results are bit-identical either way.
     block_n = 256;
     if (kvariant == 0 && mma_order == 0 && prefetch == 0 && split_mode != 2 &&
-        scheme == TCEC_SCHEME_CORRECTED3 && ex == nullptr) {
+        scheme == TCEC_SCHEME_CORRECTED3 && ex == nullptr && o.split_k <= 1) {
       int dev = 0, sms = 148;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -661,21 +703,21 @@ int sgemm_impl(int variant, int64_t m, int64_t n, int64_t k, const float* A, int
   if (variant == TCEC_FP16) {
     if (rounding == TCEC_ROUND_RN)
       return dispatch_bn<tcec::kFP16, tcec::kRN>(block_n, m, n, k, A, lda, B, ldb, C, ldc,
-                                                 scale_log2, drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, ex, d_flags, st, o.group_m);
+                                                 scale_log2, drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, ex, d_flags, st, o.group_m, o.split_k);
     if (rounding == TCEC_ROUND_RZ)
       return dispatch_bn<tcec::kFP16, tcec::kRZ>(block_n, m, n, k, A, lda, B, ldb, C, ldc,
-                                                 scale_log2, drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, ex, d_flags, st, o.group_m);
+                                                 scale_log2, drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, ex, d_flags, st, o.group_m, o.split_k);
     return TCEC_ERR_UNSUPPORTED;
   }
   if (rounding == TCEC_ROUND_RNA)
     return dispatch_bn<tcec::kTF32, tcec::kRNA>(block_n, m, n, k, A, lda, B, ldb, C, ldc, 0,
-                                                drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, ex, d_flags, st, o.group_m);
+                                                drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, ex, d_flags, st, o.group_m, o.split_k);
   if (rounding == TCEC_ROUND_RN)
     return dispatch_bn<tcec::kTF32, tcec::kRN>(block_n, m, n, k, A, lda, B, ldb, C, ldc, 0,
-                                               drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, ex, d_flags, st, o.group_m);
+                                               drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, ex, d_flags, st, o.group_m, o.split_k);
   if (rounding == TCEC_ROUND_RZ)
     return dispatch_bn<tcec::kTF32, tcec::kRZ>(block_n, m, n, k, A, lda, B, ldb, C, ldc, 0,
-                                               drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, ex, d_flags, st, o.group_m);
+                                               drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, ex, d_flags, st, o.group_m, o.split_k);
   return TCEC_ERR_UNSUPPORTED;
 }
 

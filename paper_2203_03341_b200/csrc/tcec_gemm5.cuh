@@ -64,13 +64,18 @@ __device__ __forceinline__ void pers_split_tile(uint32_t smem, uint64_t* stg_ful
   }
 }
 
-template <int V, int R>
+// kSplitK: the units of work are (tile, k part) pairs -- unit u is tile
+// u % T over operand stages [p nop / S, (p + 1) nop / S), p = u / T -- and the
+// epilogue stores the part's main-term sum and raw dC to `ws` (planes 2p and
+// 2p + 1 of m x n) for tcec_splitk_reduce_kernel instead of combining them.
+template <int V, int R, bool kSplitK = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THREADS, 1)
     tcec_gemm_pers_kernel(const __grid_constant__ CUtensorMap tmA,  // A [m][k], box 32 x 128, SW128
                           const __grid_constant__ CUtensorMap tmB,  // B [k][n], box 32 x 32, SW128
                           float* __restrict__ Cout, const int64_t ldc, const GemmShape shp,
                           const float scale, const float inv_scale, const FlagThresholds thr,
-                          uint32_t* __restrict__ flags, uint32_t* __restrict__ wave_ctr) {
+                          uint32_t* __restrict__ flags, uint32_t* __restrict__ wave_ctr,
+                          float* __restrict__ ws, const int ksplit) {
   using C = PairCfg<V>;
   using VC = VarCfg<V>;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -96,9 +101,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
   const int npairs = gridDim.x >> 1;
   const int pid = blockIdx.x >> 1;
   const int nop = shp.num_op_stages;
-  const int nstg = nop * VC::STG_PER_OP;
   const int de = shp.drain_every;
-  const int nintervals = (nop + de - 1) / de;
+  const int nparts = kSplitK ? ksplit : 1;
+  const int num_units = num_tiles * nparts;
+  // unit -> (tile, operand stages [kb0, kb1))
+  auto unit_of = [&](int u, int& tile, int& part, int& kb0, int& kb1) {
+    if constexpr (kSplitK) {
+      tile = u % num_tiles;
+      part = u / num_tiles;
+      kb0 = part * nop / nparts;
+      kb1 = (part + 1) * nop / nparts;
+    } else {
+      tile = u;
+      part = 0;
+      kb0 = 0;
+      kb1 = nop;
+    }
+  };
 
   if (warp == 0 && lane == 0) {
     if (smem_base & 1023u) __trap();
@@ -132,13 +151,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
       uint32_t gst = 0;
       uint32_t target = 0;
       int wave = 0;
-      for (int tile = pid; tile < num_tiles; tile += npairs, ++wave) {
+      for (int u = pid; u < num_units; u += npairs, ++wave) {
+        int tile, part, kb0, kb1;
+        unit_of(u, tile, part, kb0, kb1);
         if (wave_ctr != nullptr && wave > 0) {
           // lock-step waves: the CTAs that have a tile in this wave all finish
           // issuing the previous wave's loads before any starts this one, so the
           // tiles of a wave read the same k-slices while they are in L2.
           // Arrivals for wave w come from the 2 min(P, T - wP) CTAs with a wave-w tile.
-          target += 2u * static_cast<uint32_t>(min(npairs, num_tiles - wave * npairs));
+          target += 2u * static_cast<uint32_t>(min(npairs, num_units - wave * npairs));
           // The wait is bounded (~0.2 ms): the barrier only shapes L2 reuse, so a
           // CTA that cannot see its peers (e.g. not co-resident because another
           // kernel holds SMs) goes on instead of deadlocking.
@@ -154,7 +175,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
         grouped_tile(tile, tiles_m, tiles_n, shp.group_m, tm, tn);
         const int m_cta = tm * 2 * C::BM + rank * C::BM;
         const int n_cta = tn * C::BN + rank * C::BN_CTA;
-        for (int st = 0; st < nstg; ++st, ++gst) {
+        for (int st = kb0 * VC::STG_PER_OP; st < kb1 * VC::STG_PER_OP; ++st, ++gst) {
           const int s = gst % C::NSTG;
           sm100::mbar_wait(&stg_empty[s], ((gst / C::NSTG) & 1) ^ 1);
           uint8_t* dst = smem + C::OFF_STG + s * C::STG_BYTES;
@@ -174,8 +195,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
       constexpr uint32_t b_lbo_w = (uint32_t(C::B_LBO) >> 4) << 16;
       constexpr uint32_t kB = C::B_KSTEP_BYTES >> 4;
       uint32_t g = 0, git = 0, gtile = 0;
-      for (int tile = pid; tile < num_tiles; tile += npairs, ++gtile) {
-        for (int kb = 0; kb < nop; ++kb, ++g) {
+      for (int u = pid; u < num_units; u += npairs, ++gtile) {
+        int tile, part, kb0, kb1;
+        unit_of(u, tile, part, kb0, kb1);
+        const int nop_u = kb1 - kb0;
+        for (int kb = 0; kb < nop_u; ++kb, ++g) {
           const int o = g % C::NOP;
           sm100::mbar_wait_cluster(&op_full[o], (g / C::NOP) & 1);
           sm100::tc_fence_after();
@@ -205,7 +229,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
             sm100::mma_pair_split<V == kTF32>(tmem_P, ahi + 2 * ks, a_hi_w, bhi + kB * ks, b_hi_w,
                                               idesc, !(first_in_interval && ks == 0));
           sm100::mma_commit_pair_mc(&op_empty[o], 0x3);
-          if ((kb % de) == de - 1 || kb == nop - 1) {
+          if ((kb % de) == de - 1 || kb == nop_u - 1) {
             sm100::mma_commit_pair_mc(p_full, 0x3);
             ++git;
           }
@@ -218,18 +242,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
     const int t = threadIdx.x - C::SPLIT_WARP0 * 32;
     const uint32_t leader_op_full = sm100::mapa_shared(sm100::smem_u32(op_full), 0);
     uint32_t g = 0;
-    for (int tile = pid; tile < num_tiles; tile += npairs, g += nop) {
+    for (int u = pid; u < num_units; u += npairs) {
+      int tile, part, kb0, kb1;
+      unit_of(u, tile, part, kb0, kb1);
+      const int nop_u = kb1 - kb0;
       int tm, tn;
       grouped_tile(tile, tiles_m, tiles_n, shp.group_m, tm, tn);
       FlagAcc fa;
       if (flags != nullptr && (tn == 0 || tm == 0)) {
         pers_split_tile<V, R, true>(smem_base, stg_full, stg_empty, op_empty, leader_op_full, g,
-                                    nop, t, lane, scale, fa);
+                                    nop_u, t, lane, scale, fa);
         flag_publish(fa, thr, flags);
       } else {
         pers_split_tile<V, R, false>(smem_base, stg_full, stg_empty, op_empty, leader_op_full, g,
-                                     nop, t, lane, scale, fa);
+                                     nop_u, t, lane, scale, fa);
       }
+      g += nop_u;
     }
   } else {
     // setmaxnreg redistributes the launch allocation: 4 x 40 + 8 x 56 + 8 x 160 <= 20 x 96
@@ -242,7 +270,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
     const uint32_t acc_empty_leader = sm100::mapa_shared(sm100::smem_u32(acc_empty), 0);
     bool nonfinite = false;
     uint32_t git = 0;
-    for (int tile = pid; tile < num_tiles; tile += npairs) {
+    for (int u = pid; u < num_units; u += npairs) {
+      int tile, part, kb0, kb1;
+      unit_of(u, tile, part, kb0, kb1);
+      const int nintervals = (kb1 - kb0 + de - 1) / de;
       int tm, tn;
       grouped_tile(tile, tiles_m, tiles_n, shp.group_m, tm, tn);
       float acc[128];
@@ -269,6 +300,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
       const int64_t row = static_cast<int64_t>(tm) * 2 * C::BM + rank * C::BM + q * 32 + lane;
       const int col0 = tn * C::BN + h * 128;
       float* crow = Cout + row * ldc + col0;
+      if constexpr (kSplitK) {
+        // this part's main-term sum and raw dC, planes 2p / 2p + 1 (row pitch n8)
+        const int64_t n8 = (shp.n + 7) & ~7;
+        float* wc = ws + (2 * static_cast<int64_t>(part) * shp.m + row) * n8 + col0;
+        float* wd = wc + static_cast<int64_t>(shp.m) * n8;
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          uint32_t r[8];
+          sm100::tmem_ld_32x32b_x8(tmem_dC + lane_off + h * 128 + c * 8, r);
+          sm100::tmem_ld_wait();
+          const int col = col0 + c * 8;
+          if (row < shp.m && col < shp.n) {  // n8 pitch: whole 8-column groups fit
+            *reinterpret_cast<float4*>(wc + c * 8) =
+                make_float4(acc[c * 8], acc[c * 8 + 1], acc[c * 8 + 2], acc[c * 8 + 3]);
+            *reinterpret_cast<float4*>(wc + c * 8 + 4) =
+                make_float4(acc[c * 8 + 4], acc[c * 8 + 5], acc[c * 8 + 6], acc[c * 8 + 7]);
+            *reinterpret_cast<float4*>(wd + c * 8) =
+                make_float4(__uint_as_float(r[0]), __uint_as_float(r[1]), __uint_as_float(r[2]),
+                            __uint_as_float(r[3]));
+            *reinterpret_cast<float4*>(wd + c * 8 + 4) =
+                make_float4(__uint_as_float(r[4]), __uint_as_float(r[5]), __uint_as_float(r[6]),
+                            __uint_as_float(r[7]));
+          }
+        }
+      } else {
 #pragma unroll
       for (int c = 0; c < 16; ++c) {
         uint32_t r[8];
@@ -292,6 +348,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
           }
         }
       }
+      }
       // dC (and the last P) read: the next tile's MMAs may overwrite them
       sm100::tc_fence_before();
       __syncwarp();
@@ -307,6 +364,47 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
     sm100::tc_fence_after();
     sm100::tmem_dealloc_pair<C::TMEM_COLS>(tmem_base);
   }
+}
+
+// Split-K combine, one thread per 4 outputs, fixed part order (deterministic):
+// c = RN(...RN(c_0 + c_1)... + c_{S-1}), d likewise, C = RN(c + d * 2^-s) --
+// the single-pass epilogue (schemes.py:306-307) over the parts' partial sums.
+__global__ void __launch_bounds__(256)
+    tcec_splitk_reduce_kernel(const float* __restrict__ ws, int nparts, int m, int n,
+                              float* __restrict__ Cout, int64_t ldc, float inv_scale,
+                              uint32_t* __restrict__ flags) {
+  const int64_t n8 = (n + 7) & ~7;
+  const int64_t plane = static_cast<int64_t>(m) * n8;
+  const int64_t quads = static_cast<int64_t>(m) * (n8 / 4);
+  bool nonfinite = false;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < quads;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t row = i / (n8 / 4);
+    const int col = static_cast<int>(i - row * (n8 / 4)) * 4;
+    if (col >= n) continue;
+    const int64_t off = row * n8 + col;
+    float4 c = *reinterpret_cast<const float4*>(ws + off);
+    float4 d = *reinterpret_cast<const float4*>(ws + plane + off);
+    for (int p = 1; p < nparts; ++p) {
+      const float4 cp = *reinterpret_cast<const float4*>(ws + 2 * p * plane + off);
+      const float4 dp = *reinterpret_cast<const float4*>(ws + (2 * p + 1) * plane + off);
+      c.x = __fadd_rn(c.x, cp.x); c.y = __fadd_rn(c.y, cp.y);
+      c.z = __fadd_rn(c.z, cp.z); c.w = __fadd_rn(c.w, cp.w);
+      d.x = __fadd_rn(d.x, dp.x); d.y = __fadd_rn(d.y, dp.y);
+      d.z = __fadd_rn(d.z, dp.z); d.w = __fadd_rn(d.w, dp.w);
+    }
+    const float o[4] = {__fmaf_rn(d.x, inv_scale, c.x), __fmaf_rn(d.y, inv_scale, c.y),
+                        __fmaf_rn(d.z, inv_scale, c.z), __fmaf_rn(d.w, inv_scale, c.w)};
+    float* crow = Cout + row * ldc + col;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (col + j < n) {
+        crow[j] = o[j];
+        nonfinite |= !isfinite(o[j]);
+      }
+  }
+  if (flags != nullptr && __any_sync(0xFFFFFFFFu, nonfinite) && (threadIdx.x & 31) == 0)
+    atomicOr(flags, kFlagOverflow);
 }
 
 }  // namespace tcec

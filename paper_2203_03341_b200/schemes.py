@@ -282,7 +282,7 @@ def _tma_ready(t):
 def gemm_device(a, b, scheme="corrected3_halfhalf", cfg: MmaConfig | None = None, out=None,
                 flags=None, block_n: int = 0, group_m: int = 0, prefetch: int = 0,
                 kernel_variant: int = 0, drain_k: int | None = None, mma_order: int = 0,
-                split_mode: int = 0):
+                split_mode: int = 0, split_k: int = 0):
     """C = A @ B on CUDA float32 tensors, stream-ordered on torch's current stream.
 
     No host synchronisation: `flags` (int32 CUDA tensor, one element, caller
@@ -313,7 +313,8 @@ def gemm_device(a, b, scheme="corrected3_halfhalf", cfg: MmaConfig | None = None
     opts = N.make_opts(split_rounding=rounding, scale_log2=scale,
                        drain_k=dk, block_n=block_n, group_m=group_m,
                        prefetch=prefetch, kernel_variant=kernel_variant,
-                       mma_order=mma_order, split_mode=split_mode, scheme=sched)
+                       mma_order=mma_order, split_mode=split_mode, scheme=sched,
+                       split_k=split_k)
     A, lda = _tma_ready(a)
     B, ldb = _tma_ready(b)
     C, ldc = out, out.stride(0)

@@ -610,6 +610,48 @@ def test_corrected4_rn_rejects_partial_k_step():
 
 
 @pytest.mark.parametrize("sname,variant,bk,drain", VARIANTS)
+@pytest.mark.parametrize("shape,parts", [((300, 200, 1000), 3), ((1024, 1024, 1024), 4),
+                                         ((520, 576, 2048), 2), ((256, 256, 100), 8)])
+def test_split_k_vs_oracle(sname, variant, bk, drain, shape, parts):
+    """opts.split_k: k in contiguous parts, partial sums combined in part order.
+    Not the single-pass rounding sequence, so the bar is the GEMM tolerance
+    against the oracle (rows sampled across tiles), SGEMM-level accuracy
+    against FP64, determinism, and the default path's RunFlags -- including
+    inputs spanning 2^-40..2^15 (out_of_range for FP16)."""
+    import torch
+
+    T = _T()
+    m, n, k = shape
+    a = O.urand(m, k, -1, 1, m + 3 * k)
+    b = O.urand(k, n, -1, 1, n + 5 * k)
+    A, B = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    f1 = torch.zeros(1, dtype=torch.int32, device="cuda")
+    c1 = T.gemm_device(A, B, sname, split_k=parts, flags=f1)
+    c2 = T.gemm_device(A, B, sname, split_k=parts)
+    c0 = T.gemm_device(A, B, sname)
+    torch.cuda.synchronize()
+    assert torch.equal(c1, c2)  # deterministic
+    rows = np.unique(np.r_[0:4, m // 2:m // 2 + 4, m - 4:m])
+    o, _ = O.corrected3(a[rows], b, variant, block_k=bk, drain_k=drain)
+    _check_close(c1.cpu().numpy()[rows], o, a[rows], b, sname, variant)
+    ref = A.double() @ B.double()
+    r_sk = T.relative_residual(c1.double().cpu().numpy(), ref.cpu().numpy())
+    r_0 = T.relative_residual(c0.double().cpu().numpy(), ref.cpu().numpy())
+    assert r_sk <= 1.5 * r_0 + 1e-9, (r_sk, r_0)
+    assert int(f1.item()) == 0
+    # flags on wide-range inputs equal the single-pass kernel's
+    aw = O.exprand(m, k, -40, 14, m + k)
+    bw = O.exprand(k, n, -40, 14, n + k)
+    Aw, Bw = torch.from_numpy(aw).cuda(), torch.from_numpy(bw).cuda()
+    fa = torch.zeros(1, dtype=torch.int32, device="cuda")
+    fb = torch.zeros(1, dtype=torch.int32, device="cuda")
+    T.gemm_device(Aw, Bw, sname, split_k=parts, flags=fa)
+    T.gemm_device(Aw, Bw, sname, flags=fb)
+    torch.cuda.synchronize()
+    assert int(fa.item()) == int(fb.item())
+
+
+@pytest.mark.parametrize("sname,variant,bk,drain", VARIANTS)
 def test_multi_destination_epilogue(sname, variant, bk, drain):
     """tcec_sgemm_multi (the fused all-gather epilogue): every destination --
     here separate buffers on this GPU, standing in for peers' symmetric-memory
