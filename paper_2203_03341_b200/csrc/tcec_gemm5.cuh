@@ -16,6 +16,10 @@
 //     tile, so there is no shared-memory staging for a TMA store.
 //
 // C is bit-identical to the non-persistent kernel.
+//
+// With kSplitK (opts.split_k > 1) the same kernel walks (tile, k part) units
+// and stores each part's partial sums for tcec_splitk_reduce_kernel (below),
+// which combines them in a fixed part order.
 #pragma once
 
 #include "tcec_gemm2.cuh"
