@@ -71,6 +71,17 @@ def test_argument_validation_without_gpu(lib):
     assert f(0, 4, 4, 4, None, 4, None, 4, None, 4, ctypes.byref(o), None, None) == N.ERR_UNSUPPORTED
     o = N.make_opts(scale_log2=11)
     assert f(1, 4, 4, 4, None, 4, None, 4, None, 4, ctypes.byref(o), None, None) == N.ERR_UNSUPPORTED
+    # corrected4_rn blocks are whole MMA k-steps; split_k in 0..64; kernel variants 0..5
+    o = N.make_opts(scheme=4, drain_k=24)
+    assert f(0, 4, 4, 4, None, 4, None, 4, None, 4, ctypes.byref(o), None, None) == N.ERR_UNSUPPORTED
+    o = N.make_opts(scheme=4, drain_k=12)
+    assert f(1, 4, 4, 4, None, 4, None, 4, None, 4, ctypes.byref(o), None, None) == N.ERR_UNSUPPORTED
+    o = N.make_opts(split_k=65)
+    assert f(0, 4, 4, 4, None, 4, None, 4, None, 4, ctypes.byref(o), None, None) == N.ERR_UNSUPPORTED
+    o = N.make_opts(kernel_variant=6)
+    assert f(0, 4, 4, 4, None, 4, None, 4, None, 4, ctypes.byref(o), None, None) == N.ERR_UNSUPPORTED
+    o = N.make_opts(scheme=5)
+    assert f(0, 4, 4, 4, None, 4, None, 4, None, 4, ctypes.byref(o), None, None) == N.ERR_UNSUPPORTED
     s = lib.tcec_split
     assert s(3, -1, -1, None, 4, None, None, None, None) == N.ERR_ARG
     assert s(0, -1, -1, None, -4, None, None, None, None) == N.ERR_ARG
@@ -140,3 +151,29 @@ def test_c_example_runs():
                          text=True, timeout=120)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "relres" in out.stdout
+
+
+def test_scheme_routing_without_gpu():
+    """Scheme objects -> (variant, rounding, scale, product schedule), and the
+    drain interval each schedule asks for (no GPU needed)."""
+    import paper_2203_03341_b200 as T
+    from paper_2203_03341_b200 import schemes as S
+
+    assert T.resolve_schedule("corrected3_halfhalf") == (N.TCEC_FP16, N.ROUND_RN, 11, S.SCHED_CORRECTED3)
+    assert T.resolve_schedule("corrected3_tf32") == (N.TCEC_TF32, N.ROUND_RNA, 0, S.SCHED_CORRECTED3)
+    assert T.resolve_schedule("markidis4")[3] == S.SCHED_INUNIT4
+    assert T.resolve_schedule("corrected4_rz")[3] == S.SCHED_INUNIT4
+    assert T.resolve_schedule("corrected4_rn")[3] == S.SCHED_INUNIT4_RN
+    rn_tf32 = T.corrected4(T.RoundingMode.RN, T.tf32tf32())
+    assert T.resolve_schedule(rn_tf32) == (N.TCEC_TF32, N.ROUND_RNA, 0, S.SCHED_INUNIT4_RN)
+    assert T.resolve_schedule("tc_plain_fp16")[3] == S.SCHED_TC_PLAIN
+    # corrected3 drains at least the default interval in whole stages; corrected4_rn
+    # drains exactly block_k (whole MMA k-steps)
+    assert S.drain_k_for(N.TCEC_FP16, 16) == 128 and S.drain_k_for(N.TCEC_TF32, 16) == 64
+    assert S.drain_k_for(N.TCEC_FP16, 16, S.SCHED_INUNIT4_RN) == 16
+    assert S.drain_k_for(N.TCEC_TF32, 8, S.SCHED_INUNIT4_RN) == 8
+    with pytest.raises(NotImplementedError):
+        S.drain_k_for(N.TCEC_FP16, 24, S.SCHED_INUNIT4_RN)
+    for name in ("fp64_ref", "fp32_simt", "fp32_lsbtrunc"):
+        with pytest.raises(NotImplementedError):
+            T.resolve_schedule(name)
