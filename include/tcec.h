@@ -101,7 +101,9 @@ typedef struct tcec_opts {
    * part order, C = RN(sum c_p + (sum dC_p) 2^-s) -- deterministic, but not the
    * single-pass rounding sequence, so results match the reference within the
    * GEMM tolerance instead of bit for bit.  For products with fewer output
-   * tiles than SMs (small m x n, long k). */
+   * tiles than SMs (small m x n, long k).  -1 = automatic: S = min(8, idle
+   * pairs per tile, k / 1024 (FP16) or k / 512 (TF32)) when the tiles fill at
+   * most half of the CTA pairs, else off. */
   int32_t split_k;
   /* reserved[0]: L2 prefetch distance in 32-deep k-slices (0 = off);
    * reserved[1]: pair-kernel variant (0 = automatic: persistent with lock-step waves for

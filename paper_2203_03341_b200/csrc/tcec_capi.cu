@@ -672,7 +672,23 @@ int sgemm_impl(int variant, int64_t m, int64_t n, int64_t k, const float* A, int
   const int scheme = o.scheme;
   if (scheme < TCEC_SCHEME_CORRECTED3 || scheme > TCEC_SCHEME_INUNIT4_RN) return TCEC_ERR_UNSUPPORTED;
   if (in_unit && o.scale_log2 > 0) return TCEC_ERR_UNSUPPORTED;
-  if (o.split_k < 0 || o.split_k > 64) return TCEC_ERR_UNSUPPORTED;
+  if (o.split_k < -1 || o.split_k > 64) return TCEC_ERR_UNSUPPORTED;
+  if (o.split_k == -1) {
+    // automatic: split only when the 256 x 256 tiles leave most CTA pairs idle
+    // and k is long enough that each part keeps >= 16 operand stages; measured
+    // 2.2-2.7x at 1024 x 1024 x 16384, a loss on small squares
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t tiles = ((m + 255) / 256) * ((n + 255) / 256);
+    const int64_t nop = (k + (variant == TCEC_FP16 ? 63 : 31)) / (variant == TCEC_FP16 ? 64 : 32);
+    int64_t parts = tiles > 0 ? (sms / 2) / tiles : 1;
+    if (parts > nop / 16) parts = nop / 16;
+    if (parts > 8) parts = 8;
+    const bool eligible = scheme == TCEC_SCHEME_CORRECTED3 && split_mode != 2 && mma_order == 0 &&
+                          ex == nullptr && (o.block_n == 0 || o.block_n == 256);
+    o.split_k = (eligible && 2 * tiles <= sms / 2 && parts >= 2) ? static_cast<int32_t>(parts) : 0;
+  }
   if (block_n == 0) {
     // automatic tile: 256 x 192 when that tiling still fits one wave of CTA
     // pairs, so a small product keeps more SMs busy than the 256 x 256 tiling

@@ -633,6 +633,30 @@ def test_corrected4_rn_rejects_partial_k_step():
 
 
 @pytest.mark.parametrize("sname,variant,bk,drain", VARIANTS)
+def test_split_k_automatic(sname, variant, bk, drain):
+    """split_k = -1: on a long-k product with few tiles the automatic choice
+    splits (result within the GEMM tolerance, not the single-pass bits); on a
+    product that fills the GPU it stays off (bit-identical to the default)."""
+    import torch
+
+    T = _T()
+    a = O.urand(256, 16384, -1, 1, 21)
+    b = O.urand(16384, 256, -1, 1, 22)
+    A, B = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    c_auto = T.gemm_device(A, B, sname, split_k=-1)
+    c_eight = T.gemm_device(A, B, sname, split_k=8)
+    torch.cuda.synchronize()
+    assert torch.equal(c_auto, c_eight)  # 1 tile, 74 pairs, >= 16 stages per part: 8 parts
+    rows = np.r_[0:4, 250:256]
+    o, _ = O.corrected3(a[rows], b, variant, block_k=bk, drain_k=drain)
+    _check_close(c_auto.cpu().numpy()[rows], o, a[rows], b, sname, variant)
+    a2 = O.urand(4096, 512, -1, 1, 23)
+    b2 = O.urand(512, 4096, -1, 1, 24)
+    A2, B2 = torch.from_numpy(a2).cuda(), torch.from_numpy(b2).cuda()
+    assert torch.equal(T.gemm_device(A2, B2, sname, split_k=-1), T.gemm_device(A2, B2, sname))
+
+
+@pytest.mark.parametrize("sname,variant,bk,drain", VARIANTS)
 @pytest.mark.parametrize("shape,parts", [((300, 200, 1000), 3), ((1024, 1024, 1024), 4),
                                          ((520, 576, 2048), 2), ((256, 256, 100), 8)])
 def test_split_k_vs_oracle(sname, variant, bk, drain, shape, parts):

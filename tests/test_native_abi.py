@@ -76,6 +76,8 @@ def test_argument_validation_without_gpu(lib):
     assert f(0, 4, 4, 4, None, 4, None, 4, None, 4, ctypes.byref(o), None, None) == N.ERR_UNSUPPORTED
     o = N.make_opts(scheme=4, drain_k=12)
     assert f(1, 4, 4, 4, None, 4, None, 4, None, 4, ctypes.byref(o), None, None) == N.ERR_UNSUPPORTED
+    o = N.make_opts(split_k=-2)
+    assert f(0, 4, 4, 4, None, 4, None, 4, None, 4, ctypes.byref(o), None, None) == N.ERR_UNSUPPORTED
     o = N.make_opts(split_k=65)
     assert f(0, 4, 4, 4, None, 4, None, 4, None, 4, ctypes.byref(o), None, None) == N.ERR_UNSUPPORTED
     o = N.make_opts(kernel_variant=6)
