@@ -558,7 +558,12 @@ int dispatch_bn(int bn, int64_t m, int64_t n, int64_t k, const float* A, int64_t
       return launch_gemm_ts<V, R, 192, 2>(m, n, k, A, lda, B, ldb, C, ldc, s, de,
                                            gm / 2 > 0 ? gm / 2 : 1, fl, st);
     case 128:
-      return launch_gemm<V, R, 128>(m, n, k, A, lda, B, ldb, C, ldc, s, de, gm, fl, st);
+      // kernel_variant 1: the single-CTA 128 x 128 kernel (tcec_gemm.cuh, the
+      // first kernel); otherwise the CTA-pair 256 x 128 tile with A in TMEM
+      if (kv == 1) return launch_gemm<V, R, 128>(m, n, k, A, lda, B, ldb, C, ldc, s, de, gm, fl, st);
+      if (kv != 0 && kv != 4) return TCEC_ERR_UNSUPPORTED;
+      return launch_gemm_ts<V, R, 128, 4>(m, n, k, A, lda, B, ldb, C, ldc, s, de,
+                                           gm / 2 > 0 ? gm / 2 : 1, fl, st);
     default:
       return TCEC_ERR_UNSUPPORTED;
   }
@@ -690,17 +695,21 @@ int sgemm_impl(int variant, int64_t m, int64_t n, int64_t k, const float* A, int
     o.split_k = (eligible && 2 * tiles <= sms / 2 && parts >= 2) ? static_cast<int32_t>(parts) : 0;
   }
   if (block_n == 0) {
-    // automatic tile: 256 x 192 when that tiling still fits one wave of CTA
-    // pairs, so a small product keeps more SMs busy than the 256 x 256 tiling
-    // (measured +12-18% at 1024^2 and 1536^2, profiles/r01/smallbn.log); else
-    // 256 x 256.  Results are bit-identical either way.
+    // automatic tile: the narrowest of 256 x 128 / 256 x 192 whose tiling still
+    // fits one wave of CTA pairs, so a small product keeps more SMs busy than
+    // the 256 x 256 tiling (1024^2: FP16 95 / 85 / 75 TF/s for 128 / 192 / 256;
+    // 1536^2: 238 / 222 / 195; profiles/r01/smallbn.log); else 256 x 256.
+    // Results are bit-identical either way.
     block_n = 256;
     if (kvariant == 0 && mma_order == 0 && prefetch == 0 && split_mode != 2 &&
         scheme == TCEC_SCHEME_CORRECTED3 && ex == nullptr && o.split_k <= 1) {
       int dev = 0, sms = 148;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      if (((m + 255) / 256) * ((n + 191) / 192) <= sms / 2) block_n = 192;
+      if (((m + 255) / 256) * ((n + 127) / 128) <= sms / 2)
+        block_n = 128;
+      else if (((m + 255) / 256) * ((n + 191) / 192) <= sms / 2)
+        block_n = 192;
     }
   }
   if (m == 0 || n == 0) return TCEC_OK;

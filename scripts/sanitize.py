@@ -17,7 +17,8 @@ runs = []
 for sname in ("corrected3_halfhalf", "corrected3_tf32"):
     ref = T.gemm_device(A, B, sname, kernel_variant=4)
     for kw in ({}, {"kernel_variant": 2}, {"kernel_variant": 3}, {"kernel_variant": 5},
-               {"block_n": 192}, {"block_n": 128}, {"split_mode": 2}, {"mma_order": 1},
+               {"block_n": 192}, {"block_n": 128}, {"block_n": 128, "kernel_variant": 1},
+               {"split_mode": 2}, {"mma_order": 1},
                {"kernel_variant": 1}):
         c = T.gemm_device(A, B, sname, **kw)
         torch.cuda.synchronize()

@@ -401,7 +401,7 @@ def test_kernel_variants_bitwise_equal(sname, variant, bk, drain, kv):
     assert int(f0.item()) == int(f1.item())
 
 
-OPTION_SETS = [{"block_n": 192}, {"block_n": 256}, {"kernel_variant": 5}, {"mma_order": 1}, {"split_mode": 2}, {"kernel_variant": 2},
+OPTION_SETS = [{"block_n": 128}, {"block_n": 128, "kernel_variant": 1}, {"block_n": 192}, {"block_n": 256}, {"kernel_variant": 5}, {"mma_order": 1}, {"split_mode": 2}, {"kernel_variant": 2},
                {"kernel_variant": 3}, {"kernel_variant": 4}]
 
 
