@@ -77,9 +77,9 @@ typedef struct tcec_opts {
    * multiple of the operand stage depth (64 for FP16, 32 for TF32).
    * TCEC_SCHEME_INUNIT4_RN: the block of each drained product (see above). */
   int32_t drain_k;
-  /* Output tile width: 0 = automatic (the CTA-pair 256 x 256 tile, or the
-   * narrowest of 256 x 128 / 256 x 192 whose tiling fits one wave of CTA pairs;
-   * same results); 192 / 128 = CTA-pair 256 x 192 / 256 x 128 tile with the
+  /* Output tile width: 0 = automatic (the CTA-pair 256 x 256 tile, or below
+   * 8 waves of those the width among 256 / 192 / 128 with the fewest
+   * cost-weighted waves; same results); 192 / 128 = CTA-pair 256 x 192 / 256 x 128 tile with the
    * split A operand in tensor memory (128 with reserved[1] = 1: the
    * single-CTA 128 x 128 kernel). */
   int32_t block_n;

@@ -695,21 +695,33 @@ int sgemm_impl(int variant, int64_t m, int64_t n, int64_t k, const float* A, int
     o.split_k = (eligible && 2 * tiles <= sms / 2 && parts >= 2) ? static_cast<int32_t>(parts) : 0;
   }
   if (block_n == 0) {
-    // automatic tile: the narrowest of 256 x 128 / 256 x 192 whose tiling still
-    // fits one wave of CTA pairs, so a small product keeps more SMs busy than
-    // the 256 x 256 tiling (1024^2: FP16 95 / 85 / 75 TF/s for 128 / 192 / 256;
-    // 1536^2: 238 / 222 / 195; profiles/r01/smallbn.log); else 256 x 256.
-    // Results are bit-identical either way.
+    // automatic tile.  Below 8 waves of 256 x 256 tiles (the persistent
+    // kernel's range) the per-tile kernels are wave-quantised: pick the width
+    // minimising waves x width x per-flop cost, with the narrow A-from-TMEM
+    // tiles' measured costs 1.1 (256 x 192) and 1.25 (256 x 128) -- 1024^2 and
+    // 1536^2 take 128, 1792^2 and 2560^2 take 192, 2048^2 and >= 3072^2 keep
+    // 256 (profiles/r01/smallbn.log, midbn.log).  Results are bit-identical.
     block_n = 256;
     if (kvariant == 0 && mma_order == 0 && prefetch == 0 && split_mode != 2 &&
         scheme == TCEC_SCHEME_CORRECTED3 && ex == nullptr && o.split_k <= 1) {
       int dev = 0, sms = 148;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      if (((m + 255) / 256) * ((n + 127) / 128) <= sms / 2)
-        block_n = 128;
-      else if (((m + 255) / 256) * ((n + 191) / 192) <= sms / 2)
-        block_n = 192;
+      const int64_t pairs = sms / 2 > 0 ? sms / 2 : 1;
+      const int64_t rows = (m + 255) / 256;
+      if (rows * ((n + 255) / 256) < 8 * pairs) {
+        double best = 0.0;
+        const int widths[3] = {256, 192, 128};
+        const double eff[3] = {1.0, 1.1, 1.25};
+        for (int i = 0; i < 3; ++i) {
+          const int64_t waves = (rows * ((n + widths[i] - 1) / widths[i]) + pairs - 1) / pairs;
+          const double cost = double(waves) * widths[i] * eff[i];
+          if (i == 0 || cost < best) {
+            best = cost;
+            block_n = widths[i];
+          }
+        }
+      }
     }
   }
   if (m == 0 || n == 0) return TCEC_OK;
