@@ -5,7 +5,10 @@
  * This is the drop-in boundary for the reference's GEMM entry point
  * (reference: /root/reference/pkg/src/tcgemm/schemes.py).  Plain pointers and
  * sizes only; no framework types.  Every entry point is reentrant and
- * stream-ordered; results are deterministic (no atomics in any reduction of C).
+ * stream-ordered, and works on whichever device is current (per-device state:
+ * the shared-memory opt-in and occupancy are cached per kernel and device, the
+ * workspaces come from that device's stream-ordered pool); results are
+ * deterministic (no atomics in any reduction of C).
  *
  * Library: paper_2203_03341_b200/libtcec.so (nvcc, -gencode arch=compute_100a,code=sm_100a).
  */
