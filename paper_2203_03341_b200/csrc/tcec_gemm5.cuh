@@ -113,8 +113,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
     if constexpr (kSplitK) {
       tile = u % num_tiles;
       part = u / num_tiles;
-      kb0 = part * nop / nparts;
-      kb1 = (part + 1) * nop / nparts;
+      kb0 = static_cast<int>(static_cast<int64_t>(part) * nop / nparts);
+      kb1 = static_cast<int>(static_cast<int64_t>(part + 1) * nop / nparts);
     } else {
       tile = u;
       part = 0;
