@@ -701,8 +701,10 @@ int sgemm_impl(int variant, int64_t m, int64_t n, int64_t k, const float* A, int
     // tiles' measured costs 1.1 (256 x 192) and 1.25 (256 x 128) -- 1024^2 and
     // 1536^2 take 128, 1792^2 and 2560^2 take 192, 2048^2 and >= 3072^2 keep
     // 256 (profiles/r01/smallbn.log, midbn.log).  Results are bit-identical.
+    // (kernel_variant 4 -- per-tile, e.g. the host path's concurrent blocks --
+    // keeps the choice: the narrow-tile kernels are per-tile too)
     block_n = 256;
-    if (kvariant == 0 && mma_order == 0 && prefetch == 0 && split_mode != 2 &&
+    if ((kvariant == 0 || kvariant == 4) && mma_order == 0 && prefetch == 0 && split_mode != 2 &&
         scheme == TCEC_SCHEME_CORRECTED3 && ex == nullptr && o.split_k <= 1) {
       int dev = 0, sms = 148;
       cudaGetDevice(&dev);
