@@ -25,7 +25,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native as N
-from .formats import FP16, FP32, TF32, FloatFormat, RoundingMode
+from .formats import FP16, TF32, FloatFormat, RoundingMode
 from .splitting import (SplitScheme, markidis_halfhalf, native_split_args, scaled_halfhalf,
                         tf32tf32)
 

@@ -1,9 +1,7 @@
 """e2e (host buffers, pinned) through tcec_sgemm_host for several C blockings."""
 import ctypes, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np
 import torch
-import paper_2203_03341_b200 as T
 from paper_2203_03341_b200 import _native as N
 
 n = 16384

@@ -2,10 +2,8 @@
 (block_n=256) on ragged shapes, oracle spot check, then timing at large n."""
 import os
 import sys
-import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np
 import torch
 
 import paper_2203_03341_b200 as T
