@@ -773,6 +773,32 @@ def test_host_path_blockings_bit_identical(shape, blocks):
                                                         ref.flags.saw_out_of_range)
 
 
+@pytest.mark.parametrize("blocks", [(1, 1), (3, 2)])
+def test_host_path_split_k_equals_device(blocks):
+    """opts.split_k through tcec_sgemm_host: every C block splits k the same
+    way, so the blocked host result equals the device split-K result bit for bit."""
+    import ctypes
+
+    import torch
+
+    T = _T()
+    from paper_2203_03341_b200 import _native as N
+
+    m, n, k = 700, 520, 3000
+    a = O.urand(m, k, -1, 1, 31)
+    b = O.urand(k, n, -1, 1, 32)
+    ref = T.gemm_device(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), "corrected3_halfhalf",
+                        split_k=3)
+    c = np.full((m, n), np.nan, dtype=np.float32)
+    opts = N.make_opts(drain_k=0, host_blocks=blocks, split_k=3)
+    fl = ctypes.c_uint32(0)
+    N.check(N.lib().tcec_sgemm_host(N.TCEC_FP16, m, n, k, a.ctypes.data, k, b.ctypes.data, n,
+                                    c.ctypes.data, n, ctypes.byref(opts), ctypes.byref(fl), None),
+            "host")
+    assert np.array_equal(c, ref.cpu().numpy())
+    assert fl.value == 0
+
+
 @pytest.mark.parametrize("sname,variant,bk,drain", VARIANTS)
 @pytest.mark.parametrize("shape", [(16384, 16384, 16384), (65536, 1024, 1024), (2048, 2048, 65536)])
 def test_baseline_full_size_configs(sname, variant, bk, drain, shape):
