@@ -361,8 +361,9 @@ def test_large_square_properties(sname):
 @pytest.mark.parametrize("sname,variant,bk,drain", VARIANTS)
 @pytest.mark.parametrize("shape", [(256, 256, 256), (300, 520, 1000), (77, 1000, 130)])
 def test_pair_kernel_bitwise_equals_single_cta_kernel(sname, variant, bk, drain, shape):
-    """The CTA-pair 256x256 kernel (default) and the single-CTA 128x128 kernel run
-    the same per-element arithmetic: outputs and flags must be bit-identical."""
+    """The CTA-pair 256x256 kernel, the single-CTA 128x128 kernel (block_n=128,
+    kernel_variant=1) and the 256x128 A-from-TMEM pair tile (block_n=128) run the
+    same per-element arithmetic: outputs and flags must be bit-identical."""
     import torch
 
     T = _T()
@@ -373,10 +374,13 @@ def test_pair_kernel_bitwise_equals_single_cta_kernel(sname, variant, bk, drain,
     B = torch.rand((k, n), generator=g, device="cuda") * 2 - 1
     f1 = torch.zeros(1, dtype=torch.int32, device="cuda")
     f2 = torch.zeros(1, dtype=torch.int32, device="cuda")
-    c1 = T.gemm_device(A, B, sname, block_n=128, flags=f1)
+    f3 = torch.zeros(1, dtype=torch.int32, device="cuda")
+    c1 = T.gemm_device(A, B, sname, block_n=128, kernel_variant=1, flags=f1)
     c2 = T.gemm_device(A, B, sname, block_n=256, flags=f2)
+    c3 = T.gemm_device(A, B, sname, block_n=128, flags=f3)
     assert torch.equal(c1.view(torch.int32), c2.view(torch.int32))
-    assert int(f1.item()) == int(f2.item())
+    assert torch.equal(c3.view(torch.int32), c2.view(torch.int32))
+    assert int(f1.item()) == int(f2.item()) == int(f3.item())
 
 
 @pytest.mark.parametrize("kv", [1])
