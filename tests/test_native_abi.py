@@ -179,3 +179,37 @@ def test_scheme_routing_without_gpu():
     for name in ("fp64_ref", "fp32_simt", "fp32_lsbtrunc"):
         with pytest.raises(NotImplementedError):
             T.resolve_schedule(name)
+
+
+def test_no_cpu_fallback_without_library(tmp_path):
+    """With the CUDA library missing the product path raises -- it never routes
+    through the oracle or any CPU implementation."""
+    import subprocess
+    import sys
+
+    code = ("import numpy as np, paper_2203_03341_b200 as T\n"
+            "a = np.ones((4, 4), np.float32)\n"
+            "try:\n"
+            "    T.gemm(a, a, 'corrected3_tf32')\n"
+            "except RuntimeError as e:\n"
+            "    print('raised:', e)\n")
+    env = dict(os.environ, TCEC_LIB=str(tmp_path / "missing.so"))
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                         text=True, timeout=300)
+    assert "raised:" in out.stdout and "no CPU fallback" in out.stdout, out.stdout + out.stderr
+
+
+def test_no_cpu_fallback_without_gpu():
+    """Library present but no sm_100 device (this container): the call fails
+    loudly instead of computing on the host."""
+    import numpy as np
+    import torch
+
+    import paper_2203_03341_b200 as T
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    a = np.ones((4, 4), np.float32)
+    with pytest.raises(Exception):
+        T.gemm(a, a, "corrected3_tf32")
