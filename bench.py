@@ -16,7 +16,9 @@ Rank 0 prints one JSON line.  `value` is whole-job effective TFLOP/s
 API with host buffers (pinned H2D of A and B and D2H of C inside the timed
 region); `roofline` relates the GEMM kernel to the 3-product tensor roofline;
 `cpu_baseline` times the CPU oracle (a restatement of the reference's
-algorithm) on a bounded sub-block on this host.
+algorithm) on a bounded sub-block on this host; `clocks` are SM clock, power
+and throttle reasons polled through NVML every 10 ms inside the timed region
+(nvidia-smi as the fallback).
 
 --impl reference times the reference's CPU algorithm (the C oracle port, all
 host threads) on a bounded sample of the same workload and prints the same
