@@ -75,15 +75,17 @@ typedef struct tcec_opts {
   /* log2 of the residual scale: -1 = scheme default (11 FP16, 0 TF32);
    * 0 with FP16 is the unscaled markidis_halfhalf split (splitting.py:70-71). */
   int32_t scale_log2;
-  /* Drain interval of the main-term partial in k (MmaConfig.block_k,
-   * mma.py:34): 0 = default (128 for FP16, 64 for TF32); otherwise a positive
-   * multiple of the operand stage depth (64 for FP16, 32 for TF32).
+  /* Drain interval of the main-term partial in k -- the reference's
+   * MmaConfig.block_k (mma.py:34, schemes.py:300-304): 0 = default (128 for
+   * FP16, 64 for TF32); otherwise a positive multiple of the MMA k-step (16 for
+   * FP16, 8 for TF32), e.g. 16 = the reference's default schedule.  The narrow
+   * tiles (block_n 128 / 192) need a multiple of 4 k-steps.
    * TCEC_SCHEME_INUNIT4_RN: the block of each drained product (see above). */
   int32_t drain_k;
   /* Output tile width: 0 = automatic (the CTA-pair 256 x 256 tile, or below
    * 8 waves of those the width among 256 / 192 / 128 with the fewest
    * cost-weighted waves; same results); 192 / 128 = CTA-pair 256 x 192 / 256 x 128 tile with the
-   * split A operand in tensor memory (128 with reserved[1] = 1: the
+   * split A operand in tensor memory (128 with kernel_variant = 1: the
    * single-CTA 128 x 128 kernel). */
   int32_t block_n;
   /* Tile rasterisation group along m in 128-row tiles: 0 = default (8). */
@@ -110,13 +112,13 @@ typedef struct tcec_opts {
    * pairs per tile, k / 1024 (FP16) or k / 512 (TF32)) when the tiles fill at
    * most half of the CTA pairs, else off. */
   int32_t split_k;
-  /* reserved[0]: L2 prefetch distance in 32-deep k-slices (0 = off);
-   * reserved[1]: pair-kernel variant (0 = automatic: persistent with lock-step waves for
-   *              products of >= 8 waves of tiles, else per-tile; 1 = unified split/drain
-   *              workers; 2 = persistent; 3 = persistent, lock-step waves; 4 = per-tile;
-   *              5 = persistent clusters of two pairs sharing the split of A -- slower);
-   * reserved[2]: pair-kernel MMA order (0 = corrections first, 1 = A_hi collector reuse). */
-  int32_t reserved[3];
+  /* Kernel: 0 = automatic (persistent with lock-step waves for products of
+   * >= 8 waves of 256 x 256 tiles, else per-tile); 1 = the single-CTA kernel
+   * (block_n 128 only); 2 = persistent; 3 = persistent with lock-step waves;
+   * 4 = per-tile (for a kernel sharing the GPU with other work).  Results are
+   * bit-identical across kernels. */
+  int32_t kernel_variant;
+  int32_t reserved[2];
 } tcec_opts;
 
 /* Library version (major * 10000 + minor * 100 + patch). */
@@ -159,6 +161,10 @@ int tcec_sgemm_multi(int variant, int64_t m, int64_t n, int64_t k, const float* 
 int tcec_sgemm_host(int variant, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda,
                     const float* B, int64_t ldb, float* C, int64_t ldc, const tcec_opts* opts,
                     uint32_t* h_flags, void* stream);
+
+/* Frees the device copies of A, B and C that tcec_sgemm_host keeps cached on
+ * the current device between calls (its streams and events stay). */
+int tcec_host_release(void);
 
 /* Elementwise split of count FP32 values (splitting.py:114-122 _split_arrays,
  * split_matrix :139-147): hi and lo are written as FP32 values (FP16 values

@@ -12,7 +12,7 @@ import os
 import subprocess
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# TCEC_LIB may point at a measurement build of the same library (make -C csrc exp)
+# TCEC_LIB may point at another build of the same library
 LIB_PATH = os.environ.get("TCEC_LIB") or os.path.join(_HERE, "libtcec.so")
 CSRC = os.path.join(_HERE, "csrc")
 
@@ -32,6 +32,7 @@ EXPORTS = (
     "tcec_split",
     "tcec_split_census",
     "tcec_launch_count",
+    "tcec_host_release",
 )
 
 
@@ -47,7 +48,8 @@ class TcecOpts(ctypes.Structure):
         ("host_row_blocks", ctypes.c_int32),
         ("host_col_blocks", ctypes.c_int32),
         ("split_k", ctypes.c_int32),
-        ("reserved", ctypes.c_int32 * 3),
+        ("kernel_variant", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 2),
     ]
 
 
@@ -92,6 +94,7 @@ def lib() -> ctypes.CDLL:
     L.tcec_split.restype = i32
     L.tcec_split.argtypes = [i32, i32, i32, p, i64, p, p, p, p]
     L.tcec_launch_count.restype = u64
+    L.tcec_host_release.restype = i32
     _lib = L
     return L
 
@@ -109,17 +112,15 @@ def check(status: int, what: str) -> None:
 
 
 def make_opts(split_rounding: int = ROUND_DEFAULT, scale_log2: int = -1, drain_k: int = 0,
-              block_n: int = 0, group_m: int = 0, prefetch: int = 0,
-              kernel_variant: int = 0, mma_order: int = 0, split_mode: int = 0,
-              scheme: int = 0, host_blocks: tuple = (0, 0), split_k: int = 0) -> TcecOpts:
+              block_n: int = 0, group_m: int = 0, kernel_variant: int = 0,
+              split_mode: int = 0, scheme: int = 0, host_blocks: tuple = (0, 0),
+              split_k: int = 0) -> TcecOpts:
     o = TcecOpts()
     o.split_k = split_k
     o.host_row_blocks, o.host_col_blocks = host_blocks
     o.split_mode = split_mode
     o.scheme = scheme
-    o.reserved[0] = prefetch
-    o.reserved[1] = kernel_variant
-    o.reserved[2] = mma_order
+    o.kernel_variant = kernel_variant
     o.split_rounding = split_rounding
     o.scale_log2 = scale_log2
     o.drain_k = drain_k

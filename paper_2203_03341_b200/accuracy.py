@@ -82,11 +82,11 @@ def _flags_field(saw_overflow: bool, saw_out_of_range: bool) -> str:
     return ";".join(parts)
 
 
-def gemm_accuracy(ms, ns, ks, schemes, dist, seeds, block_k: int = 16) -> list[str]:
+def gemm_accuracy(ms, ns, ks, schemes, dist, seeds, block_k: int = 0) -> list[str]:
     """cmd_gemm_accuracy (cli.py:135-170) with the GEMMs on the GPU."""
     import torch
 
-    from .schemes import MmaConfig, gemm
+    from .schemes import gemm
 
     for name in schemes:
         if name not in GPU_SCHEMES:
@@ -95,7 +95,7 @@ def gemm_accuracy(ms, ns, ks, schemes, dist, seeds, block_k: int = 16) -> list[s
         raise ValueError("no schemes requested")
     prev_tf32 = torch.backends.cuda.matmul.allow_tf32
     torch.backends.cuda.matmul.allow_tf32 = False
-    cfg = MmaConfig(block_k=block_k)
+    cfg = _cfg(block_k)
     lines = ["m,n,k,scheme,seed,residual,flags"]
     try:
         for m in ms:
@@ -135,6 +135,14 @@ def gemm_accuracy(ms, ns, ks, schemes, dist, seeds, block_k: int = 16) -> list[s
     return lines
 
 
+def _cfg(block_k: int):
+    """block_k > 0: MmaConfig(block_k), the reference's drain schedule; 0: the
+    kernel's tuned default drain interval (no MmaConfig)."""
+    from .schemes import MmaConfig
+
+    return MmaConfig(block_k=block_k) if block_k > 0 else None
+
+
 def _residual(ref, out) -> float:
     """analysis.py:175-192 (Eq. 7) against the FP64 product on the GPU."""
     import torch
@@ -154,32 +162,32 @@ def _sizes_seeds(ms, ns, ks, seeds, dist, what):
                     yield m, n, k, seed
 
 
-def ablate_delta(ms, ns, ks, dist, seeds, block_k: int = 16) -> list[str]:
+def ablate_delta(ms, ns, ks, dist, seeds, block_k: int = 0) -> list[str]:
     """cmd_ablate_delta (cli.py:196-214) on the tensor core."""
     import torch
 
-    from .schemes import MmaConfig, delta_term_ablation
+    from .schemes import delta_term_ablation
 
     lines = ["m,n,k,seed,residual_3term,residual_4term,max_ulp_diff"]
     for m, n, k, seed in _sizes_seeds(ms, ns, ks, seeds, dist, "ablate-delta"):
         a, b = input_pair(dist, m, n, k, seed)
         ref = torch.from_numpy(a).cuda().double() @ torch.from_numpy(b).cuda().double()
-        run3, run4, max_ulp = delta_term_ablation(a, b, cfg=MmaConfig(block_k=block_k))
+        run3, run4, max_ulp = delta_term_ablation(a, b, cfg=_cfg(block_k))
         lines.append(f"{m},{n},{k},{seed},{_fmt64(_residual(ref, run3.output))},"
                      f"{_fmt64(_residual(ref, run4.output))},{_fmt64(max_ulp)}")
     return lines
 
 
-def rounding_ablation(ms, ns, ks, dist, seeds, block_k: int = 16) -> list[str]:
+def rounding_ablation(ms, ns, ks, dist, seeds, block_k: int = 0) -> list[str]:
     """Hardware analogue of cmd_rounding_ablation (cli.py:173-193): the in-unit
     four-term scheme with the tensor core's own terminal rounding against
     corrected3 (main-term accumulation moved out of the unit, RN adds) and
     cuBLAS SGEMM."""
     import torch
 
-    from .schemes import MmaConfig, gemm
+    from .schemes import gemm
 
-    cfg = MmaConfig(block_k=block_k)
+    cfg = _cfg(block_k)
     prev_tf32 = torch.backends.cuda.matmul.allow_tf32
     torch.backends.cuda.matmul.allow_tf32 = False
     lines = ["m,n,k,seed,residual_inunit_hw,residual_corrected3,residual_fp32"]
@@ -246,7 +254,8 @@ def _add_size_flags(p, default_k: str) -> None:
     p.add_argument("--n", default="16")
     p.add_argument("--k", default=default_k)
     p.add_argument("--seeds", default="0,1,2,3,4,5,6,7")
-    p.add_argument("--block-k", type=int, default=16, help="drain interval request (MmaConfig.block_k)")
+    p.add_argument("--block-k", type=int, default=0,
+                   help="main-term drain interval, MmaConfig.block_k (0 = the kernel's default)")
 
 
 def _build_parser() -> argparse.ArgumentParser:

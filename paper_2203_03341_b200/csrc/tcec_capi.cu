@@ -19,10 +19,8 @@
 #include "tcec.h"
 #include "tcec_gemm.cuh"
 #include "tcec_gemm2.cuh"
-#include "tcec_gemm3.cuh"
 #include "tcec_gemm4.cuh"
 #include "tcec_gemm5.cuh"
-#include "tcec_gemm6.cuh"
 #include "tcec_presplit.cuh"
 #include "tcec_census.cuh"
 
@@ -153,8 +151,6 @@ int launch_gemm(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, co
   shp.num_op_stages = static_cast<int32_t>((k + VC::BK_OP - 1) / VC::BK_OP);
   shp.drain_every = drain_every;
   shp.group_m = group_m;
-  shp.prefetch = 0;
-  shp.mma_order = 0;
   const float scale = ldexpf(1.0f, scale_log2);
   const float inv_scale = ldexpf(1.0f, -scale_log2);
   const tcec::FlagThresholds thr = tcec::flag_thresholds(V, R, scale_log2);
@@ -165,11 +161,10 @@ int launch_gemm(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, co
   return cudaGetLastError() == cudaSuccess ? TCEC_OK : TCEC_ERR_CUDA;
 }
 
-template <int V, int R, bool kUnified>
+template <int V, int R>
 int launch_gemm_pair(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, const float* B,
                      int64_t ldb, float* C, int64_t ldc, int scale_log2, int drain_every,
-                     int group_m, int prefetch, int mma_order, const ExtraC* ex,
-                     uint32_t* d_flags, cudaStream_t stream) {
+                     int group_m, const ExtraC* ex, uint32_t* d_flags, cudaStream_t stream) {
   using Cfg = tcec::PairCfg<V>;
   using VC = tcec::VarCfg<V>;
   CUtensorMap tmA, tmB, tmC;
@@ -185,7 +180,7 @@ int launch_gemm_pair(int64_t m, int64_t n, int64_t k, const float* A, int64_t ld
     if ((st = make_tmap(&cx.m[d], ex->c[d], n, m, ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B)))
       return st;
 
-  auto kern = kUnified ? tcec::tcec_gemm_pair_uni_kernel<V, R> : tcec::tcec_gemm_pair_kernel<V, R>;
+  auto kern = tcec::tcec_gemm_pair_kernel<V, R>;
   const cudaError_t attr_err = smem_optin(kern, Cfg::SMEM_BYTES);
   if (attr_err != cudaSuccess) return TCEC_ERR_CUDA;
 
@@ -196,8 +191,6 @@ int launch_gemm_pair(int64_t m, int64_t n, int64_t k, const float* A, int64_t ld
   shp.num_op_stages = static_cast<int32_t>((k + VC::BK_OP - 1) / VC::BK_OP);
   shp.drain_every = drain_every;
   shp.group_m = group_m;
-  shp.prefetch = prefetch;
-  shp.mma_order = mma_order;
   const float scale = ldexpf(1.0f, scale_log2);
   const float inv_scale = ldexpf(1.0f, -scale_log2);
   const tcec::FlagThresholds thr = tcec::flag_thresholds(V, R, scale_log2);
@@ -232,8 +225,6 @@ int launch_gemm_ts(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda,
   shp.num_op_stages = static_cast<int32_t>((k + VC::BK_OP - 1) / VC::BK_OP);
   shp.drain_every = drain_every;
   shp.group_m = group_m;
-  shp.prefetch = 0;
-  shp.mma_order = 0;
   const float scale = ldexpf(1.0f, scale_log2);
   const float inv_scale = ldexpf(1.0f, -scale_log2);
   const tcec::FlagThresholds thr = tcec::flag_thresholds(V, R, scale_log2);
@@ -312,8 +303,6 @@ int launch_gemm_presplit(int64_t m, int64_t n, int64_t k, const float* A, int64_
     shp.num_op_stages = static_cast<int32_t>((k + VC::BK_OP - 1) / VC::BK_OP);
     shp.drain_every = drain_every;
     shp.group_m = group_user > 0 ? group_m : (lockstep ? 8 : group_m);
-    shp.prefetch = 0;
-    shp.mma_order = 0;
     kern<<<static_cast<unsigned>(2 * pairs), Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream>>>(
         tmAh, tmAl, tmBh, tmBl, C, ldc, shp, inv_scale, inv_scale2, d_flags, wave_ctr);
     g_launches.fetch_add(3, std::memory_order_relaxed);
@@ -351,8 +340,6 @@ int launch_gemm_pers(int64_t m, int64_t n, int64_t k, const float* A, int64_t ld
   shp.num_op_stages = static_cast<int32_t>((k + VC::BK_OP - 1) / VC::BK_OP);
   shp.drain_every = drain_every;
   shp.group_m = group_m;
-  shp.prefetch = 0;
-  shp.mma_order = 0;
   const float scale = ldexpf(1.0f, scale_log2);
   const float inv_scale = ldexpf(1.0f, -scale_log2);
   const tcec::FlagThresholds thr = tcec::flag_thresholds(V, R, scale_log2);
@@ -409,165 +396,148 @@ int launch_gemm_pers(int64_t m, int64_t n, int64_t k, const float* A, int64_t ld
   return launched ? TCEC_OK : TCEC_ERR_CUDA;
 }
 
-// Persistent CTA-quad kernel (kernel_variant 5): two pairs per cluster of four
-// share the split of A (tcec_gemm6.cuh).  The grid is the number of co-resident
-// clusters of four (GPCs with an odd number of TPCs leave one idle).
-template <int V, int R>
-int launch_gemm_quad(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, const float* B,
-                     int64_t ldb, float* C, int64_t ldc, int scale_log2, int drain_every,
-                     int group_m, bool lockstep_ok, uint32_t* d_flags, cudaStream_t stream) {
-  using Cfg = tcec::QuadCfg<V>;
-  using VC = tcec::VarCfg<V>;
-  CUtensorMap tmA, tmB;
-  int st;
-  if ((st = make_tmap(&tmA, A, k, m, lda, Cfg::BK_STG, Cfg::A_ROWS, CU_TENSOR_MAP_SWIZZLE_128B)))
-    return st;
-  if ((st = make_tmap(&tmB, B, n, k, ldb, 32, Cfg::BK_STG, CU_TENSOR_MAP_SWIZZLE_128B))) return st;
-  auto kern = tcec::tcec_gemm_quad_kernel<V, R>;
-  const cudaError_t attr_err = smem_optin(kern, Cfg::SMEM_BYTES);
-  // co-resident clusters of four, per device
-  static std::mutex occ_mu;
-  static int occ_quads[64] = {0};
-  int max_quads = 0;
-  if (attr_err == cudaSuccess) {
-    int d = 0;
-    cudaGetDevice(&d);
-    std::lock_guard<std::mutex> lk(occ_mu);
-    if (d >= 0 && d < 64 && occ_quads[d] == 0) {
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(4, 1, 1);
-      cfg.blockDim = dim3(Cfg::NUM_THREADS, 1, 1);
-      cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
-      if (cudaOccupancyMaxActiveClusters(&occ_quads[d], kern, &cfg) != cudaSuccess) {
-        cudaGetLastError();
-        occ_quads[d] = -1;
-      }
-    }
-    if (d >= 0 && d < 64) max_quads = occ_quads[d];
-  }
-  if (attr_err != cudaSuccess) return TCEC_ERR_CUDA;
+int device_sms() {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  tcec::GemmShape shp;
-  shp.m = static_cast<int32_t>(m);
-  shp.n = static_cast<int32_t>(n);
-  shp.k = static_cast<int32_t>(k);
-  shp.num_op_stages = static_cast<int32_t>((k + VC::BK_OP - 1) / VC::BK_OP);
-  shp.drain_every = drain_every;
-  shp.group_m = group_m;
-  shp.prefetch = 0;
-  shp.mma_order = 0;
-  const float scale = ldexpf(1.0f, scale_log2);
-  const float inv_scale = ldexpf(1.0f, -scale_log2);
-  const tcec::FlagThresholds thr = tcec::flag_thresholds(V, R, scale_log2);
-  const int64_t tiles_n = (n + Cfg::BN - 1) / Cfg::BN;
-  const int64_t units = ((m + 2 * Cfg::BM - 1) / (2 * Cfg::BM)) * ((tiles_n + 1) / 2);
-  int64_t quads = max_quads > 0 ? max_quads : sms / 4 - 4;
-  if (quads > units) quads = units;
-  if (quads < 1) quads = 1;
-  const bool lockstep = lockstep_ok && units >= 8 * quads;
-  uint32_t* wave_ctr = nullptr;
-  if (lockstep) {
-    keep_pool(dev);
-    if (cudaMallocAsync(reinterpret_cast<void**>(&wave_ctr), sizeof(uint32_t), stream) != cudaSuccess)
-      return TCEC_ERR_CUDA;
-    if (cudaMemsetAsync(wave_ctr, 0, sizeof(uint32_t), stream) != cudaSuccess) {
-      cudaFreeAsync(wave_ctr, stream);
-      return TCEC_ERR_CUDA;
-    }
-  }
-  kern<<<static_cast<unsigned>(4 * quads), Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream>>>(
-      tmA, tmB, C, ldc, shp, scale, inv_scale, thr, d_flags, wave_ctr);
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  const bool launched = cudaGetLastError() == cudaSuccess;
-  if (wave_ctr) cudaFreeAsync(wave_ctr, stream);
-  return launched ? TCEC_OK : TCEC_ERR_CUDA;
+  return sms;
 }
 
+// Resolved options of one call (sgemm_impl -> dispatch).
+struct Plan {
+  int block_n;        // 256 / 192 / 128
+  int kvariant;       // 1 single-CTA (block_n 128), 2 persistent, 3 lock-step, 4 per-tile
+  int kv_user;        // as requested (0 = automatic)
+  int split_mode;     // 0 / 1 fused, 2 split-once
+  int scheme;         // TCEC_SCHEME_*
+  int split_k;        // parts (<= 1: off)
+  int drain_every;    // MMA k-steps per drain interval (corrected3) / per block (INUNIT4_RN)
+  int group_m;        // rasterisation group in 128-row tiles
+  int group_user;     // the caller's group_m (0 = default)
+  int scale_log2;
+};
+
 template <int V, int R>
-int dispatch_bn(int bn, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda,
-                const float* B, int64_t ldb, float* C, int64_t ldc, int s, int de, int gm, int pf,
-                int kv, int mo, int sm, int sch, const ExtraC* ex, uint32_t* fl,
-                cudaStream_t st, int gm_user, int sk = 0) {
-  if (ex && ex->count > 0 && (bn != 256 || sm == 2 || sch != TCEC_SCHEME_CORRECTED3))
-    return TCEC_ERR_UNSUPPORTED;  // extra destinations: the default pair kernels only
-  if (sk > 1) {  // split-K: the persistent pair kernel over (tile, part) units
-    if (sm == 2 || sch != TCEC_SCHEME_CORRECTED3 || (ex && ex->count > 0) || mo != 0 ||
-        (bn != 256 && bn != 0))
+int dispatch(const Plan& p, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda,
+             const float* B, int64_t ldb, float* C, int64_t ldc, const ExtraC* ex, uint32_t* fl,
+             cudaStream_t st) {
+  const int s = p.scale_log2, de = p.drain_every, kv = p.kvariant, gm = p.group_m;
+  const int gpair = gm / 2 > 0 ? gm / 2 : 1;  // group in pair-tile rows
+  const bool extra = ex && ex->count > 0;
+  if (extra && (p.block_n != 256 || p.split_mode == 2 || p.scheme != TCEC_SCHEME_CORRECTED3 ||
+                p.split_k > 1 || kv != 4))
+    return TCEC_ERR_UNSUPPORTED;  // extra destinations: the per-tile pair kernel only
+  if (p.split_k > 1) {  // split-K: the persistent pair kernel over (tile, part) units
+    if (p.split_mode == 2 || p.scheme != TCEC_SCHEME_CORRECTED3 || p.block_n != 256)
       return TCEC_ERR_UNSUPPORTED;
-    const int g = gm_user > 0 ? (gm / 2 > 0 ? gm / 2 : 1) : 8;
-    // lock-step waves unless the caller pinned the per-tile variant (the host
-    // path's concurrent blocks)
-    return launch_gemm_pers<V, R>(m, n, k, A, lda, B, ldb, C, ldc, s, de, g, kv != 4, fl, st, sk);
+    const int g = p.group_user > 0 ? gpair : 8;
+    // lock-step waves unless the caller pinned the per-tile variant (a kernel
+    // sharing the GPU with other work, e.g. the host path's concurrent blocks)
+    return launch_gemm_pers<V, R>(m, n, k, A, lda, B, ldb, C, ldc, s, de, g, p.kv_user != 4, fl,
+                                  st, p.split_k);
   }
-  if (sm == 2 || sch != TCEC_SCHEME_CORRECTED3) {
-    if ((bn != 256 && bn != 0) || (kv != 0 && kv != 4) || mo != 0) return TCEC_ERR_UNSUPPORTED;
-    const int g = gm / 2 > 0 ? gm / 2 : 1;
-    const bool ls = kv != 4;  // the host path's concurrent blocks pin variant 4
-    switch (sch) {
+  if (p.split_mode == 2 || p.scheme != TCEC_SCHEME_CORRECTED3) {
+    if (p.block_n != 256 || (p.kv_user != 0 && p.kv_user != 4)) return TCEC_ERR_UNSUPPORTED;
+    const bool ls = p.kv_user != 4;  // lock-step waves once the product spans >= 8 of them
+    const int gu = p.group_user;
+    switch (p.scheme) {
       case TCEC_SCHEME_CORRECTED3:
-        return launch_gemm_presplit<V, R, tcec::kSchC3>(m, n, k, A, lda, B, ldb, C, ldc, s, de, g, gm_user, ls, fl, st);
+        return launch_gemm_presplit<V, R, tcec::kSchC3>(m, n, k, A, lda, B, ldb, C, ldc, s, de, gpair, gu, ls, fl, st);
       case TCEC_SCHEME_CORRECTED3_DD:
-        return launch_gemm_presplit<V, R, tcec::kSchC3DD>(m, n, k, A, lda, B, ldb, C, ldc, s, de, g, gm_user, ls, fl, st);
+        return launch_gemm_presplit<V, R, tcec::kSchC3DD>(m, n, k, A, lda, B, ldb, C, ldc, s, de, gpair, gu, ls, fl, st);
       case TCEC_SCHEME_TC_PLAIN:
-        return launch_gemm_presplit<V, R, tcec::kSchPlain>(m, n, k, A, lda, B, ldb, C, ldc, 0, de, g, gm_user, ls, fl, st);
+        return launch_gemm_presplit<V, R, tcec::kSchPlain>(m, n, k, A, lda, B, ldb, C, ldc, 0, de, gpair, gu, ls, fl, st);
       case TCEC_SCHEME_INUNIT4:
-        return launch_gemm_presplit<V, R, tcec::kSchIn4>(m, n, k, A, lda, B, ldb, C, ldc, s, de, g, gm_user, ls, fl, st);
+        return launch_gemm_presplit<V, R, tcec::kSchIn4>(m, n, k, A, lda, B, ldb, C, ldc, s, de, gpair, gu, ls, fl, st);
       case TCEC_SCHEME_INUNIT4_RN:  // de = MMA k-steps per drained block
-        return launch_gemm_presplit<V, R, tcec::kSchIn4RN>(m, n, k, A, lda, B, ldb, C, ldc, s, de, g, gm_user, ls, fl, st);
+        return launch_gemm_presplit<V, R, tcec::kSchIn4RN>(m, n, k, A, lda, B, ldb, C, ldc, s, de, gpair, gu, ls, fl, st);
       default:
         return TCEC_ERR_UNSUPPORTED;
     }
   }
-  switch (bn) {
-    case 256: {
-      // kernel_variant 0 = automatic: the persistent kernel with lock-step waves
-      // of 8 x 9 pair tiles once the product spans >= 8 waves (measured +2-8% at
-      // 8192^3 .. 32768 x 16384^2, DRAM reads -21..-52%), else the per-tile kernel
-      const int64_t tiles = ((m + 255) / 256) * ((n + 255) / 256);
-      int sms = 148;
-      {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      }
-      if (kv == 0)
-        kv = (tiles >= 8 * int64_t(sms / 2) && !(ex && ex->count > 0) && mo == 0 && pf == 0) ? 3
-                                                                                         : 4;
-      if (kv == 2 || kv == 3) {  // persistent; 3 = with lock-step waves
-        if (ex && ex->count > 0) return TCEC_ERR_UNSUPPORTED;
-        const int g = gm_user > 0 ? (gm / 2 > 0 ? gm / 2 : 1) : (kv == 3 ? 8 : 4);
-        return launch_gemm_pers<V, R>(m, n, k, A, lda, B, ldb, C, ldc, s, de, g, kv == 3, fl, st);
-      }
-      if (kv == 5) {  // persistent CTA quads sharing the A split
-        if (ex && ex->count > 0) return TCEC_ERR_UNSUPPORTED;
-        const int g = gm_user > 0 ? (gm / 2 > 0 ? gm / 2 : 1) : 8;
-        return launch_gemm_quad<V, R>(m, n, k, A, lda, B, ldb, C, ldc, s, de, g, true, fl, st);
-      }
-      if (kv == 4) kv = 0;  // the per-tile pair kernel
-      if (kv == 1)
-        return launch_gemm_pair<V, R, true>(m, n, k, A, lda, B, ldb, C, ldc, s, de,
-                                            gm / 2 > 0 ? gm / 2 : 1, pf, mo, ex, fl, st);
-      if (kv != 0) return TCEC_ERR_UNSUPPORTED;
-      return launch_gemm_pair<V, R, false>(m, n, k, A, lda, B, ldb, C, ldc, s, de,
-                                           gm / 2 > 0 ? gm / 2 : 1, pf, mo, ex, fl, st);
+  if (p.block_n == 256) {
+    if (kv == 2 || kv == 3) {  // persistent; 3 = with lock-step waves
+      const int g = p.group_user > 0 ? gpair : (kv == 3 ? 8 : 4);
+      return launch_gemm_pers<V, R>(m, n, k, A, lda, B, ldb, C, ldc, s, de, g, kv == 3, fl, st);
     }
-    case 192:
-      if (kv != 0 && kv != 4) return TCEC_ERR_UNSUPPORTED;
-      return launch_gemm_ts<V, R, 192, 2>(m, n, k, A, lda, B, ldb, C, ldc, s, de,
-                                           gm / 2 > 0 ? gm / 2 : 1, fl, st);
-    case 128:
-      // kernel_variant 1: the single-CTA 128 x 128 kernel (tcec_gemm.cuh, the
-      // first kernel); otherwise the CTA-pair 256 x 128 tile with A in TMEM
-      if (kv == 1) return launch_gemm<V, R, 128>(m, n, k, A, lda, B, ldb, C, ldc, s, de, gm, fl, st);
-      if (kv != 0 && kv != 4) return TCEC_ERR_UNSUPPORTED;
-      return launch_gemm_ts<V, R, 128, 4>(m, n, k, A, lda, B, ldb, C, ldc, s, de,
-                                           gm / 2 > 0 ? gm / 2 : 1, fl, st);
-    default:
-      return TCEC_ERR_UNSUPPORTED;
+    if (kv != 4) return TCEC_ERR_UNSUPPORTED;
+    return launch_gemm_pair<V, R>(m, n, k, A, lda, B, ldb, C, ldc, s, de, gpair, ex, fl, st);
   }
+  // the narrow tiles run whole operand stages per drain interval
+  if (de % 4 != 0) return TCEC_ERR_UNSUPPORTED;
+  if (p.block_n == 192) {
+    if (kv != 4) return TCEC_ERR_UNSUPPORTED;
+    return launch_gemm_ts<V, R, 192, 2>(m, n, k, A, lda, B, ldb, C, ldc, s, de, gpair, fl, st);
+  }
+  if (p.block_n == 128) {
+    // kernel_variant 1: the single-CTA 128 x 128 kernel (tcec_gemm.cuh, the
+    // first kernel); otherwise the CTA-pair 256 x 128 tile with A in TMEM
+    if (kv == 1) return launch_gemm<V, R, 128>(m, n, k, A, lda, B, ldb, C, ldc, s, de, gm, fl, st);
+    if (kv != 4) return TCEC_ERR_UNSUPPORTED;
+    return launch_gemm_ts<V, R, 128, 4>(m, n, k, A, lda, B, ldb, C, ldc, s, de, gpair, fl, st);
+  }
+  return TCEC_ERR_UNSUPPORTED;
 }
+
+// Per-device resources of the host-buffer entry (tcec_sgemm_host), kept
+// across calls: four streams, the block events and device copies of A, B, C
+// (grown on demand, freed by tcec_host_release).  One call at a time per
+// device (the mutex); the call itself is synchronous.
+constexpr int kMaxDevices = 64;
+struct HostCtx {
+  static constexpr int kMaxBlk = 8;
+  std::mutex mu;
+  bool ready = false;
+  cudaStream_t s_in = nullptr, s_out = nullptr, s_c[2] = {nullptr, nullptr};
+  cudaEvent_t ev_start = nullptr, ev_a[kMaxBlk] = {}, ev_b[kMaxBlk] = {},
+              ev_g[kMaxBlk * kMaxBlk] = {};
+  float *dA = nullptr, *dB = nullptr, *dC = nullptr;
+  size_t capA = 0, capB = 0, capC = 0;  // floats
+  uint32_t* dF = nullptr;
+
+  cudaError_t init() {
+    cudaError_t e;
+    for (cudaStream_t* x : {&s_in, &s_out, &s_c[0], &s_c[1]})
+      if ((e = cudaStreamCreateWithFlags(x, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming)) != cudaSuccess) return e;
+    for (int i = 0; i < kMaxBlk; ++i) {
+      if ((e = cudaEventCreateWithFlags(&ev_a[i], cudaEventDisableTiming)) != cudaSuccess) return e;
+      if ((e = cudaEventCreateWithFlags(&ev_b[i], cudaEventDisableTiming)) != cudaSuccess) return e;
+    }
+    for (int i = 0; i < kMaxBlk * kMaxBlk; ++i)
+      if ((e = cudaEventCreateWithFlags(&ev_g[i], cudaEventDisableTiming)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(reinterpret_cast<void**>(&dF), sizeof(uint32_t))) != cudaSuccess) return e;
+    ready = true;
+    return cudaSuccess;
+  }
+  static cudaError_t grow(float*& p, size_t& cap, size_t need) {
+    if (need <= cap) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    const cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&p), need * sizeof(float));
+    if (e == cudaSuccess) cap = need;
+    return e;
+  }
+  cudaError_t reserve(size_t a, size_t b, size_t c) {
+    cudaError_t e;
+    if ((e = grow(dA, capA, a)) != cudaSuccess) return e;
+    if ((e = grow(dB, capB, b)) != cudaSuccess) return e;
+    return grow(dC, capC, c);
+  }
+  cudaError_t release() {
+    cudaError_t e = cudaSuccess;
+    for (float** p : {&dA, &dB, &dC})
+      if (*p) {
+        const cudaError_t f = cudaFree(*p);
+        if (e == cudaSuccess) e = f;
+        *p = nullptr;
+      }
+    capA = capB = capC = 0;
+    return e;
+  }
+};
+HostCtx g_host[kMaxDevices];
 
 int resolve_rounding(int variant, int rounding) {
   if (rounding == TCEC_ROUND_DEFAULT) return variant == TCEC_FP16 ? TCEC_ROUND_RN : TCEC_ROUND_RNA;
@@ -638,93 +608,88 @@ int sgemm_impl(int variant, int64_t m, int64_t n, int64_t k, const float* A, int
   const int rounding = resolve_rounding(variant, o.split_rounding);
   if (!rounding_supported(variant, rounding)) return TCEC_ERR_UNSUPPORTED;
   const bool in_unit = o.scheme == TCEC_SCHEME_INUNIT4 || o.scheme == TCEC_SCHEME_INUNIT4_RN;
-  int scale_log2 = o.scale_log2 < 0 ? (variant == TCEC_FP16 && !in_unit &&
-                                        o.scheme != TCEC_SCHEME_TC_PLAIN ? 11 : 0)
-                                     : o.scale_log2;
-  if (variant == TCEC_TF32 && scale_log2 != 0) return TCEC_ERR_UNSUPPORTED;
-  if (variant == TCEC_FP16 && scale_log2 != 0 && scale_log2 != 11) return TCEC_ERR_UNSUPPORTED;
-  const int bk_op = variant == TCEC_FP16 ? 64 : 32;
-  // default drain interval: 128 (FP16) / 64 (TF32) -- measured both faster and
-  // more accurate against FP64 than draining every operand stage
-  int drain_every = 2;
-  if (o.scheme == TCEC_SCHEME_INUNIT4_RN) {
-    // the drained block is the reference's block_k, in MMA k-steps (16 / 8 deep)
-    const int kstep = variant == TCEC_FP16 ? 16 : 8;
-    const int bk = o.drain_k == 0 ? 16 : o.drain_k;
-    if (bk < 0 || bk % kstep != 0) return TCEC_ERR_UNSUPPORTED;
-    drain_every = bk / kstep;
-  } else if (o.drain_k != 0) {
-    if (o.drain_k < 0 || o.drain_k % bk_op != 0) return TCEC_ERR_UNSUPPORTED;
-    drain_every = o.drain_k / bk_op;
-  }
-  int block_n = o.block_n;
-  if (block_n != 0 && block_n != 128 && block_n != 192 && block_n != 256)
+  Plan p;
+  p.scale_log2 = o.scale_log2 < 0 ? (variant == TCEC_FP16 && !in_unit &&
+                                     o.scheme != TCEC_SCHEME_TC_PLAIN ? 11 : 0)
+                                  : o.scale_log2;
+  if (variant == TCEC_TF32 && p.scale_log2 != 0) return TCEC_ERR_UNSUPPORTED;
+  if (variant == TCEC_FP16 && p.scale_log2 != 0 && p.scale_log2 != 11) return TCEC_ERR_UNSUPPORTED;
+  if (o.scheme < TCEC_SCHEME_CORRECTED3 || o.scheme > TCEC_SCHEME_INUNIT4_RN)
     return TCEC_ERR_UNSUPPORTED;
-  const int group_m = o.group_m <= 0 ? 8 : o.group_m;
-  // reserved[0]: L2 prefetch distance in 32-deep k-slices (pair kernel; 0 = off)
-  const int prefetch = o.reserved[0] < 0 ? 0 : (o.reserved[0] > 16 ? 16 : o.reserved[0]);
-  // reserved[1]: pair-kernel variant (0 = automatic, 1 = unified split/drain workers,
-  // 2 = persistent, 3 = persistent with lock-step waves, 4 = per-tile)
-  const int kvariant = o.reserved[1];
-  if (kvariant < 0 || kvariant > 5) return TCEC_ERR_UNSUPPORTED;
-  // reserved[2]: pair-kernel MMA order (0 = corrections then main term, 1 = A_hi collector reuse)
-  const int mma_order = o.reserved[2];
-  if (mma_order != 0 && mma_order != 1) return TCEC_ERR_UNSUPPORTED;
-  // split_mode: 0 / 1 = split fused into the GEMM, 2 = split once in a separate pass
-  const int split_mode = o.split_mode;
-  if (split_mode < 0 || split_mode > 2) return TCEC_ERR_UNSUPPORTED;
-  // scheme: product schedule (TCEC_SCHEME_*); the comparators run in split-once mode
-  const int scheme = o.scheme;
-  if (scheme < TCEC_SCHEME_CORRECTED3 || scheme > TCEC_SCHEME_INUNIT4_RN) return TCEC_ERR_UNSUPPORTED;
   if (in_unit && o.scale_log2 > 0) return TCEC_ERR_UNSUPPORTED;
+  p.scheme = o.scheme;
+  // Drain interval in MMA k-steps (16 deep FP16, 8 deep TF32).  corrected3:
+  // the main-term block of schemes.py:300-304, default 128 (FP16) / 64 (TF32)
+  // -- measured both faster and more accurate against FP64 than draining every
+  // operand stage; INUNIT4_RN: the reference's block_k, default 16.
+  const int kstep = variant == TCEC_FP16 ? 16 : 8;
+  const int drain_k = o.drain_k != 0 ? o.drain_k
+                                     : (o.scheme == TCEC_SCHEME_INUNIT4_RN ? 16 : 8 * kstep);
+  if (drain_k <= 0 || drain_k % kstep != 0) return TCEC_ERR_UNSUPPORTED;
+  p.drain_every = drain_k / kstep;
+  if (o.block_n != 0 && o.block_n != 128 && o.block_n != 192 && o.block_n != 256)
+    return TCEC_ERR_UNSUPPORTED;
+  // the narrow tiles drain whole operand stages (4 k-steps)
+  if ((o.block_n == 128 || o.block_n == 192) && p.drain_every % 4 != 0) return TCEC_ERR_UNSUPPORTED;
+  p.group_user = o.group_m;
+  p.group_m = o.group_m <= 0 ? 8 : o.group_m;
+  // kernel_variant: 0 = automatic, 1 = single-CTA (block_n 128), 2 = persistent,
+  // 3 = persistent with lock-step waves, 4 = per-tile
+  p.kvariant = p.kv_user = o.kernel_variant;
+  if (p.kvariant < 0 || p.kvariant > 4) return TCEC_ERR_UNSUPPORTED;
+  if (p.kvariant == 1 && o.block_n != 128) return TCEC_ERR_UNSUPPORTED;
+  // split_mode: 0 / 1 = split fused into the GEMM, 2 = split once in a separate pass
+  p.split_mode = o.split_mode;
+  if (p.split_mode < 0 || p.split_mode > 2) return TCEC_ERR_UNSUPPORTED;
   if (o.split_k < -1 || o.split_k > 64) return TCEC_ERR_UNSUPPORTED;
-  if (o.split_k == -1) {
+  const bool fused_c3 = p.scheme == TCEC_SCHEME_CORRECTED3 && p.split_mode != 2;
+  const int sms = device_sms();
+  const int64_t pairs = sms / 2 > 0 ? sms / 2 : 1;
+  const int64_t tiles256 = ((m + 255) / 256) * ((n + 255) / 256);
+  p.split_k = o.split_k;
+  if (p.split_k == -1) {
     // automatic: split only when the 256 x 256 tiles leave most CTA pairs idle
     // and k is long enough that each part keeps >= 16 operand stages; measured
     // 2.2-2.7x at 1024 x 1024 x 16384, a loss on small squares
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t tiles = ((m + 255) / 256) * ((n + 255) / 256);
     const int64_t nop = (k + (variant == TCEC_FP16 ? 63 : 31)) / (variant == TCEC_FP16 ? 64 : 32);
-    int64_t parts = tiles > 0 ? (sms / 2) / tiles : 1;
+    int64_t parts = tiles256 > 0 ? pairs / tiles256 : 1;
     if (parts > nop / 16) parts = nop / 16;
     if (parts > 8) parts = 8;
-    const bool eligible = scheme == TCEC_SCHEME_CORRECTED3 && split_mode != 2 && mma_order == 0 &&
-                          ex == nullptr && (o.block_n == 0 || o.block_n == 256);
-    o.split_k = (eligible && 2 * tiles <= sms / 2 && parts >= 2) ? static_cast<int32_t>(parts) : 0;
+    const bool eligible = fused_c3 && ex == nullptr && (o.block_n == 0 || o.block_n == 256) &&
+                          p.kvariant != 1;
+    p.split_k = (eligible && 2 * tiles256 <= pairs && parts >= 2) ? static_cast<int>(parts) : 0;
   }
-  if (block_n == 0) {
+  p.block_n = o.block_n;
+  if (p.block_n == 0) {
     // automatic tile.  Below 8 waves of 256 x 256 tiles (the persistent
     // kernel's range) the per-tile kernels are wave-quantised: pick the width
     // minimising waves x width x per-flop cost, with the narrow A-from-TMEM
     // tiles' measured costs 1.1 (256 x 192) and 1.25 (256 x 128) -- 1024^2 and
     // 1536^2 take 128, 1792^2 and 2560^2 take 192, 2048^2 and >= 3072^2 keep
     // 256 (profiles/r01/smallbn.log, midbn.log).  Results are bit-identical.
-    // (kernel_variant 4 -- per-tile, e.g. the host path's concurrent blocks --
-    // keeps the choice: the narrow-tile kernels are per-tile too)
-    block_n = 256;
-    if ((kvariant == 0 || kvariant == 4) && mma_order == 0 && prefetch == 0 && split_mode != 2 &&
-        scheme == TCEC_SCHEME_CORRECTED3 && ex == nullptr && o.split_k <= 1) {
-      int dev = 0, sms = 148;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      const int64_t pairs = sms / 2 > 0 ? sms / 2 : 1;
+    // The narrow tiles drain per operand stage (multiples of 4 k-steps).
+    p.block_n = 256;
+    if ((p.kvariant == 0 || p.kvariant == 4) && fused_c3 && ex == nullptr && p.split_k <= 1 &&
+        p.drain_every % 4 == 0 && tiles256 < 8 * pairs) {
       const int64_t rows = (m + 255) / 256;
-      if (rows * ((n + 255) / 256) < 8 * pairs) {
-        double best = 0.0;
-        const int widths[3] = {256, 192, 128};
-        const double eff[3] = {1.0, 1.1, 1.25};
-        for (int i = 0; i < 3; ++i) {
-          const int64_t waves = (rows * ((n + widths[i] - 1) / widths[i]) + pairs - 1) / pairs;
-          const double cost = double(waves) * widths[i] * eff[i];
-          if (i == 0 || cost < best) {
-            best = cost;
-            block_n = widths[i];
-          }
+      double best = 0.0;
+      const int widths[3] = {256, 192, 128};
+      const double eff[3] = {1.0, 1.1, 1.25};
+      for (int i = 0; i < 3; ++i) {
+        const int64_t waves = (rows * ((n + widths[i] - 1) / widths[i]) + pairs - 1) / pairs;
+        const double cost = double(waves) * widths[i] * eff[i];
+        if (i == 0 || cost < best) {
+          best = cost;
+          p.block_n = widths[i];
         }
       }
     }
+  }
+  if (p.kvariant == 0) {
+    // automatic kernel: the persistent kernel with lock-step waves of 8 x 9
+    // pair tiles once a 256 x 256 product spans >= 8 waves (measured +2-8% at
+    // 8192^3 .. 32768 x 16384^2, DRAM reads -21..-52%), else per-tile
+    p.kvariant = (p.block_n == 256 && fused_c3 && ex == nullptr && tiles256 >= 8 * pairs) ? 3 : 4;
   }
   if (m == 0 || n == 0) return TCEC_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -739,24 +704,20 @@ int sgemm_impl(int variant, int64_t m, int64_t n, int64_t k, const float* A, int
   int s;
   if ((s = check_arch())) return s;
   if ((s = get_encoder())) return s;
+  using namespace tcec;
   if (variant == TCEC_FP16) {
     if (rounding == TCEC_ROUND_RN)
-      return dispatch_bn<tcec::kFP16, tcec::kRN>(block_n, m, n, k, A, lda, B, ldb, C, ldc,
-                                                 scale_log2, drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, ex, d_flags, st, o.group_m, o.split_k);
+      return dispatch<kFP16, kRN>(p, m, n, k, A, lda, B, ldb, C, ldc, ex, d_flags, st);
     if (rounding == TCEC_ROUND_RZ)
-      return dispatch_bn<tcec::kFP16, tcec::kRZ>(block_n, m, n, k, A, lda, B, ldb, C, ldc,
-                                                 scale_log2, drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, ex, d_flags, st, o.group_m, o.split_k);
+      return dispatch<kFP16, kRZ>(p, m, n, k, A, lda, B, ldb, C, ldc, ex, d_flags, st);
     return TCEC_ERR_UNSUPPORTED;
   }
   if (rounding == TCEC_ROUND_RNA)
-    return dispatch_bn<tcec::kTF32, tcec::kRNA>(block_n, m, n, k, A, lda, B, ldb, C, ldc, 0,
-                                                drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, ex, d_flags, st, o.group_m, o.split_k);
+    return dispatch<kTF32, kRNA>(p, m, n, k, A, lda, B, ldb, C, ldc, ex, d_flags, st);
   if (rounding == TCEC_ROUND_RN)
-    return dispatch_bn<tcec::kTF32, tcec::kRN>(block_n, m, n, k, A, lda, B, ldb, C, ldc, 0,
-                                               drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, ex, d_flags, st, o.group_m, o.split_k);
+    return dispatch<kTF32, kRN>(p, m, n, k, A, lda, B, ldb, C, ldc, ex, d_flags, st);
   if (rounding == TCEC_ROUND_RZ)
-    return dispatch_bn<tcec::kTF32, tcec::kRZ>(block_n, m, n, k, A, lda, B, ldb, C, ldc, 0,
-                                               drain_every, group_m, prefetch, kvariant, mma_order, split_mode, scheme, ex, d_flags, st, o.group_m, o.split_k);
+    return dispatch<kTF32, kRZ>(p, m, n, k, A, lda, B, ldb, C, ldc, ex, d_flags, st);
   return TCEC_ERR_UNSUPPORTED;
 }
 
@@ -802,14 +763,23 @@ int tcec_sgemm_host(int variant, int64_t m, int64_t n, int64_t k, const float* A
   // down on the copy-out stream as soon as it is done.  So the GEMM starts after
   // 1/R of A and 1/Cb of B instead of after all of B, and the download overlaps
   // the remaining uploads.  Rows and columns are independent, so the result is
-  // bit-identical to one launch over the whole product.
+  // bit-identical to one launch over the whole product.  Streams, events and
+  // device buffers are cached per device (HostCtx) across calls.
   if (m < 0 || n < 0 || k < 0) return TCEC_ERR_ARG;
   if (lda < (k > 0 ? k : 1) || ldb < (n > 0 ? n : 1) || ldc < (n > 0 ? n : 1)) return TCEC_ERR_ARG;
   if (h_flags) *h_flags = 0;
   if (m == 0 || n == 0) return TCEC_OK;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return TCEC_ERR_CUDA;
-  keep_pool(dev);
+  if (dev < 0 || dev >= kMaxDevices) return TCEC_ERR_CUDA;
+  HostCtx& H = g_host[dev];
+  std::lock_guard<std::mutex> lk(H.mu);
+  int status = TCEC_OK;
+  auto cu = [&](cudaError_t e) {
+    if (e != cudaSuccess && status == TCEC_OK) status = TCEC_ERR_CUDA;
+    return e == cudaSuccess;
+  };
+  if (!H.ready && !cu(H.init())) return status;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t dlda = ((k > 0 ? k : 1) + 3) / 4 * 4;
   const int64_t dldb = (n + 3) / 4 * 4;
@@ -821,7 +791,7 @@ int tcec_sgemm_host(int variant, int64_t m, int64_t n, int64_t k, const float* A
   auto blocks = [](int64_t extent, int requested, int cap) {
     int64_t nb = requested > 0 ? requested : (extent + 2047) / 2048;
     if (requested <= 0 && nb > cap) nb = cap;
-    if (nb > 8) nb = 8;
+    if (nb > HostCtx::kMaxBlk) nb = HostCtx::kMaxBlk;
     if (nb < 1) nb = 1;
     int64_t sz = ((extent + nb - 1) / nb + 255) / 256 * 256;
     return sz < 256 ? int64_t(256) : sz;
@@ -833,36 +803,19 @@ int tcec_sgemm_host(int variant, int64_t m, int64_t n, int64_t k, const float* A
   bo.split_rounding = TCEC_ROUND_DEFAULT;
   bo.scale_log2 = -1;
   if (opts) bo = *opts;
-  if (bo.reserved[1] == 0) bo.reserved[1] = 4;
+  if (bo.kernel_variant == 0) bo.kernel_variant = 4;
   const int64_t rb = blocks(m, opts ? opts->host_row_blocks : 0, 8);
   const int64_t cbk = blocks(n, opts ? opts->host_col_blocks : 0, variant == TCEC_FP16 ? 4 : 8);
   const int R = static_cast<int>((m + rb - 1) / rb);
   const int Cb = static_cast<int>((n + cbk - 1) / cbk);
-  float *dA = nullptr, *dB = nullptr, *dC = nullptr;
-  uint32_t* dF = nullptr;
-  cudaStream_t s_in = nullptr, s_out = nullptr, s_c[2] = {nullptr, nullptr};
-  cudaEvent_t ev_start = nullptr;
-  cudaEvent_t ev_a[8] = {}, ev_b[8] = {}, ev_g[64] = {};
-  int status = TCEC_OK;
-  auto cu = [&](cudaError_t e) {
-    if (e != cudaSuccess && status == TCEC_OK) status = TCEC_ERR_CUDA;
-    return e == cudaSuccess;
-  };
-  bool ok = cu(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking)) &&
-            cu(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking)) &&
-            cu(cudaStreamCreateWithFlags(&s_c[0], cudaStreamNonBlocking)) &&
-            cu(cudaStreamCreateWithFlags(&s_c[1], cudaStreamNonBlocking)) &&
-            cu(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
-  for (int i = 0; ok && i < R; ++i) ok = cu(cudaEventCreateWithFlags(&ev_a[i], cudaEventDisableTiming));
-  for (int j = 0; ok && j < Cb; ++j) ok = cu(cudaEventCreateWithFlags(&ev_b[j], cudaEventDisableTiming));
-  for (int b = 0; ok && b < R * Cb; ++b) ok = cu(cudaEventCreateWithFlags(&ev_g[b], cudaEventDisableTiming));
-  ok = ok && cu(cudaMallocAsync(reinterpret_cast<void**>(&dA), size_t(m) * dlda * sizeof(float), st)) &&
-       cu(cudaMallocAsync(reinterpret_cast<void**>(&dB), size_t(kk) * dldb * sizeof(float), st)) &&
-       cu(cudaMallocAsync(reinterpret_cast<void**>(&dC), size_t(m) * dldc * sizeof(float), st)) &&
-       cu(cudaMallocAsync(reinterpret_cast<void**>(&dF), sizeof(uint32_t), st)) &&
-       cu(cudaMemsetAsync(dF, 0, sizeof(uint32_t), st)) && cu(cudaEventRecord(ev_start, st));
-  for (cudaStream_t x : {s_in, s_out, s_c[0], s_c[1]})
-    if (ok) ok = cu(cudaStreamWaitEvent(x, ev_start, 0));  // allocations are ordered on st
+  bool ok = cu(H.reserve(size_t(m) * dlda, size_t(kk) * dldb, size_t(m) * dldc)) &&
+            cu(cudaMemsetAsync(H.dF, 0, sizeof(uint32_t), st)) &&
+            cu(cudaEventRecord(H.ev_start, st));
+  float* const dA = H.dA;
+  float* const dB = H.dB;
+  float* const dC = H.dC;
+  for (cudaStream_t x : {H.s_in, H.s_out, H.s_c[0], H.s_c[1]})
+    if (ok) ok = cu(cudaStreamWaitEvent(x, H.ev_start, 0));  // prior work on `stream`
   // uploads, interleaved A_0 B_0 A_1 B_1 ...
   for (int s = 0; ok && s < (R > Cb ? R : Cb); ++s) {
     if (s < R) {
@@ -870,15 +823,15 @@ int tcec_sgemm_host(int variant, int64_t m, int64_t n, int64_t k, const float* A
       if (k > 0)
         ok = cu(cudaMemcpy2DAsync(dA + r0 * dlda, dlda * sizeof(float), A + r0 * lda,
                                   lda * sizeof(float), k * sizeof(float), rows,
-                                  cudaMemcpyHostToDevice, s_in));
-      ok = ok && cu(cudaEventRecord(ev_a[s], s_in));
+                                  cudaMemcpyHostToDevice, H.s_in));
+      ok = ok && cu(cudaEventRecord(H.ev_a[s], H.s_in));
     }
     if (ok && s < Cb) {
       const int64_t c0 = s * cbk, cols = (c0 + cbk <= n) ? cbk : n - c0;
       if (k > 0)
         ok = cu(cudaMemcpy2DAsync(dB + c0, dldb * sizeof(float), B + c0, ldb * sizeof(float),
-                                  cols * sizeof(float), k, cudaMemcpyHostToDevice, s_in));
-      ok = ok && cu(cudaEventRecord(ev_b[s], s_in));
+                                  cols * sizeof(float), k, cudaMemcpyHostToDevice, H.s_in));
+      ok = ok && cu(cudaEventRecord(H.ev_b[s], H.s_in));
     }
   }
   // GEMM blocks in arrival order, downloads as they complete
@@ -891,44 +844,38 @@ int tcec_sgemm_host(int variant, int64_t m, int64_t n, int64_t k, const float* A
         const int i = pass == 0 ? s : t, j = pass == 0 ? t : s;
         const int64_t r0 = i * rb, rows = (r0 + rb <= m) ? rb : m - r0;
         const int64_t c0 = j * cbk, cols = (c0 + cbk <= n) ? cbk : n - c0;
-        cudaStream_t sc = s_c[launched & 1];
-        ok = cu(cudaStreamWaitEvent(sc, ev_a[i], 0)) && cu(cudaStreamWaitEvent(sc, ev_b[j], 0));
+        cudaStream_t sc = H.s_c[launched & 1];
+        ok = cu(cudaStreamWaitEvent(sc, H.ev_a[i], 0)) && cu(cudaStreamWaitEvent(sc, H.ev_b[j], 0));
         if (!ok) break;
         const int s2 = tcec_sgemm(variant, rows, cols, k, dA + r0 * dlda, dlda, dB + c0, dldb,
-                                  dC + r0 * dldc + c0, dldc, &bo, dF, sc);
+                                  dC + r0 * dldc + c0, dldc, &bo, H.dF, sc);
         if (s2 != TCEC_OK) {
           status = s2;
           ok = false;
           break;
         }
-        cudaEvent_t eg = ev_g[launched];
-        ok = cu(cudaEventRecord(eg, sc)) && cu(cudaStreamWaitEvent(s_out, eg, 0)) &&
+        cudaEvent_t eg = H.ev_g[launched];
+        ok = cu(cudaEventRecord(eg, sc)) && cu(cudaStreamWaitEvent(H.s_out, eg, 0)) &&
              cu(cudaMemcpy2DAsync(C + r0 * ldc + c0, ldc * sizeof(float), dC + r0 * dldc + c0,
                                   dldc * sizeof(float), cols * sizeof(float), rows,
-                                  cudaMemcpyDeviceToHost, s_out));
+                                  cudaMemcpyDeviceToHost, H.s_out));
         ++launched;
       }
     }
   }
   if (ok && h_flags)  // s_out has waited on every block's GEMM
-    cu(cudaMemcpyAsync(h_flags, dF, sizeof(uint32_t), cudaMemcpyDeviceToHost, s_out));
-  for (cudaStream_t x : {s_out, s_in, s_c[0], s_c[1]})
-    if (x) cu(cudaStreamSynchronize(x));
-  if (dA) cudaFreeAsync(dA, st);
-  if (dB) cudaFreeAsync(dB, st);
-  if (dC) cudaFreeAsync(dC, st);
-  if (dF) cudaFreeAsync(dF, st);
-  cu(cudaStreamSynchronize(st));
-  for (int i = 0; i < 8; ++i) {
-    if (ev_a[i]) cudaEventDestroy(ev_a[i]);
-    if (ev_b[i]) cudaEventDestroy(ev_b[i]);
-  }
-  for (int b = 0; b < 64; ++b)
-    if (ev_g[b]) cudaEventDestroy(ev_g[b]);
-  if (ev_start) cudaEventDestroy(ev_start);
-  for (cudaStream_t x : {s_in, s_out, s_c[0], s_c[1]})
-    if (x) cudaStreamDestroy(x);
+    cu(cudaMemcpyAsync(h_flags, H.dF, sizeof(uint32_t), cudaMemcpyDeviceToHost, H.s_out));
+  for (cudaStream_t x : {H.s_out, H.s_in, H.s_c[0], H.s_c[1]}) cu(cudaStreamSynchronize(x));
   return status;
+}
+
+int tcec_host_release(void) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return TCEC_ERR_CUDA;
+  if (dev < 0 || dev >= kMaxDevices) return TCEC_ERR_CUDA;
+  HostCtx& H = g_host[dev];
+  std::lock_guard<std::mutex> lk(H.mu);
+  return H.release() == cudaSuccess ? TCEC_OK : TCEC_ERR_CUDA;
 }
 
 int tcec_split_census(int kind, int rounding, int e_v, unsigned long long* d_counts,

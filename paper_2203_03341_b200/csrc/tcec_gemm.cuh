@@ -29,10 +29,8 @@ namespace tcec {
 struct GemmShape {
   int32_t m, n, k;
   int32_t num_op_stages;   // ceil(k / BK_OP)
-  int32_t drain_every;     // operand stages per drain interval (>= 1)
+  int32_t drain_every;     // MMA k-steps (16 FP16 / 8 TF32 deep) per drain interval (>= 1)
   int32_t group_m;         // tile rasterisation group
-  int32_t prefetch;        // L2 prefetch distance in staging slices (0 = off)
-  int32_t mma_order;       // pair kernel: 1 = A_hi reuse through the MMA collector
 };
 
 // Extra destinations of the output tile (fused all-gather: this rank's C slab
@@ -217,7 +215,7 @@ __global__ void __launch_bounds__(TileCfg<BN>::NUM_THREADS, 1)
   const int n0 = tile_n * BN;
   const int nop = shp.num_op_stages;
   const int nstg = nop * VC::STG_PER_OP;
-  const int de = shp.drain_every;
+  const int de = shp.drain_every / 4;  // operand stages per drain interval (host: a multiple of 4 k-steps)
 
   // ---- one-time setup
   if (warp == 0 && lane == 0) {

@@ -21,14 +21,6 @@
 
 #include "tcec_gemm.cuh"
 
-// Measurement-only builds (make exp; results are garbage): bit 1 = split warps
-// store constants instead of splitting, bit 2 = drain warps skip the TMEM
-// reads, bit 4 = no TMA loads (staging left stale), bit 8 = split warps skip
-// the staging reads (LDS).  Used to attribute time.
-#ifndef TCEC_EXP
-#define TCEC_EXP 0
-#endif
-
 namespace tcec {
 
 template <int V>
@@ -70,6 +62,48 @@ struct PairCfg {
   static_assert(NUM_DRAIN_WARPS * EPI_WARP_BYTES <= OFF_BAR, "epilogue staging reuses the rings");
 };
 
+// The MMAs of one operand stage (4 MMA k-steps) of the corrected3 schedule.
+// corr(ks) issues k-step ks's correction products into dC (schemes.py:294-298);
+// mainp(ks, acc) its main product into P.  P is drained every `de` k-steps --
+// the main-term block of schemes.py:300-304 with block_k = de x MMA-K: the
+// first main product of an interval waits until the drain warps have read the
+// previous interval (p_empty) and starts from zero, the last one commits
+// p_full.  j0 is the stage's first k-step within the unit of work, nks the
+// unit's k-steps, git the interval counter (running across tiles).  With
+// stage-aligned intervals the stage's corrections go first, so the drain of
+// the previous P overlaps them; otherwise each k-step's corrections precede its
+// main product.  The order of products into each accumulator is the same
+// either way.
+template <typename Corr, typename Main>
+__device__ __forceinline__ void c3_stage(int j0, int nks, int de, uint32_t& git, uint64_t* p_empty,
+                                         uint64_t* p_full, Corr corr, Main mainp) {
+  auto main_step = [&](int ks) {
+    const int j = j0 + ks;
+    const bool first = j % de == 0;
+    if (first && git > 0) {
+      sm100::mbar_wait_cluster(p_empty, (git - 1) & 1);
+      sm100::tc_fence_after();
+    }
+    mainp(ks, first ? 0u : 1u);
+    if (j % de == de - 1 || j == nks - 1) {
+      sm100::mma_commit_pair_mc(p_full, 0x3);
+      ++git;
+    }
+  };
+  if (de % 4 == 0) {
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) corr(ks);
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) main_step(ks);
+  } else {
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      corr(ks);
+      main_step(ks);
+    }
+  }
+}
+
 // Split one 32-deep FP32 slice of this CTA's A rows and B columns into the
 // operand stage (all addresses are 32-bit shared-window addresses).
 // Thread t (0..255):
@@ -89,6 +123,10 @@ __device__ __forceinline__ void split16(const float (&x)[16], float scale, uint3
       float h0, h1, r0, r1;
       unpack_f16x2(hw[j], h0, h1);
       sm100::residual_x2(x[2 * j], x[2 * j + 1], h0, h1, scale, r0, r1);
+      // splitting.py:119-121: lo = 0 where hi overflowed (the residual
+      // formula would give -+inf or NaN there)
+      r0 = isinf(h0) ? 0.0f : r0;
+      r1 = isinf(h1) ? 0.0f : r1;
       lw[j] = cvt_f16x2<R>(r0, r1);
     }
   } else {
@@ -96,8 +134,10 @@ __device__ __forceinline__ void split16(const float (&x)[16], float scale, uint3
     for (int j = 0; j < 16; j += 2) {
       hw[j] = tf32_round_bits<R>(__float_as_uint(x[j]));
       hw[j + 1] = tf32_round_bits<R>(__float_as_uint(x[j + 1]));
+      // splitting.py:119-121: where hi overflowed the residual is x - x = 0
+      const float h0 = __uint_as_float(hw[j]), h1 = __uint_as_float(hw[j + 1]);
       float r0, r1;
-      sm100::sub_x2(x[j], x[j + 1], __uint_as_float(hw[j]), __uint_as_float(hw[j + 1]), r0, r1);
+      sm100::sub_x2(x[j], x[j + 1], isinf(h0) ? x[j] : h0, isinf(h1) ? x[j + 1] : h1, r0, r1);
       lw[j] = tf32_round_bits<R>(__float_as_uint(r0));
       lw[j + 1] = tf32_round_bits<R>(__float_as_uint(r1));
     }
@@ -160,11 +200,7 @@ __device__ __forceinline__ void pair_split_part(uint32_t stg, uint32_t op, int s
     const int half = t >> 7;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-#if TCEC_EXP & 8
-      const float4 v = make_float4(__int_as_float(t * 7 + i), 1.5f + i, 2.5f, -0.75f * half);
-#else
       const float4 v = sm100::lds128(stg + sw128(row, half * 4 + i));
-#endif
       x[4 * i] = v.x; x[4 * i + 1] = v.y; x[4 * i + 2] = v.z; x[4 * i + 3] = v.w;
     }
     chunk_first = V == kFP16 ? sub * 4 + half * 2 : half * 4;
@@ -179,11 +215,7 @@ __device__ __forceinline__ void pair_split_part(uint32_t stg, uint32_t op, int s
     const int h = V == kTF32 ? (t >> 2) & 1 : 0;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-#if TCEC_EXP & 8
-      const float4 v = make_float4(__int_as_float(t * 5 + i), 0.5f + i, 3.5f, -1.25f * qn);
-#else
       const float4 v = sm100::lds128(box + sw128(row, (qn & 1) * 4 + (i ^ h)));
-#endif
       x[4 * i] = v.x; x[4 * i + 1] = v.y; x[4 * i + 2] = v.z; x[4 * i + 3] = v.w;
     }
     chunk_first = ((qn * 16) % C::B_ATOM_N) * (V == kFP16 ? 2 : 4) / 16;
@@ -194,11 +226,6 @@ __device__ __forceinline__ void pair_split_part(uint32_t stg, uint32_t op, int s
   }
   const uint32_t hi_base = op + (kB ? 2 * C::OP_A_BYTES : 0);
   const uint32_t lo_base = hi_base + (kB ? C::OP_B_BYTES : C::OP_A_BYTES);
-#if TCEC_EXP & 1
-  sm100::sts128(hi_base + sw128(t & 127, sub * 4 + (t >> 7) * 2), 0x3c003c00u, 0, 0, 0);
-  sm100::sts128(lo_base + sw128(t & 127, sub * 4 + (t >> 7) * 2), 0x3c003c00u, 0, 0, 0);
-  return;
-#endif
   uint32_t hw[16], lw[16];
   split16<V, R>(x, scale, hw, lw);
   constexpr int NCH = V == kFP16 ? 2 : 4;  // 16-byte chunks per 16 values
@@ -245,10 +272,8 @@ __device__ __forceinline__ void pair_split_loop(uint32_t smem, uint64_t* stg_ful
       sm100::mbar_wait(&stg_full[s], (st / C::NSTG) & 1);
       if (sub == 0) sm100::mbar_wait(&op_empty[o], ((kb / C::NOP) & 1) ^ 1);
       const uint32_t stg = smem + C::OFF_STG + s * C::STG_BYTES;
-      if (!((TCEC_EXP & 16) && (st & 1))) {
-        pair_split_part<V, R, kFlags, false>(stg, op, sub, t, scale, fa);
-        pair_split_part<V, R, kFlags, true>(stg, op, sub, t, scale, fa);
-      }
+      pair_split_part<V, R, kFlags, false>(stg, op, sub, t, scale, fa);
+      pair_split_part<V, R, kFlags, true>(stg, op, sub, t, scale, fa);
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(&stg_empty[s]);
     }
@@ -306,8 +331,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
   const int n_cta = n_pair + rank * C::BN_CTA;            // this CTA's B columns
   const int nop = shp.num_op_stages;
   const int nstg = nop * VC::STG_PER_OP;
-  const int de = shp.drain_every;
-  const int nintervals = (nop + de - 1) / de;
+  const int de = shp.drain_every;  // MMA k-steps per drain interval
+  const int nintervals = (4 * nop + de - 1) / de;
 
   if (warp == 0 && lane == 0) {
     if (smem_base & 1023u) __trap();  // SW128 operand atoms need 1024-byte alignment
@@ -338,37 +363,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
     sm100::regs_dec<40>();
     if (warp == 0 && lane == 0) {
       // ===================== TMA producer =====================
-      // L2 prefetch runs kPrefetch slices ahead of the staging ring so the ring's
-      // loads hit L2 instead of paying DRAM latency.
-      const int kPrefetch = shp.prefetch;
-      auto prefetch = [&](int sp) {
-        if (sp < nstg) {
-          sm100::tma_prefetch_2d(&tmA, sp * C::BK_STG, m_cta);
-#pragma unroll
-          for (int b = 0; b < 4; ++b) sm100::tma_prefetch_2d(&tmB, n_cta + 32 * b, sp * C::BK_STG);
-        }
-      };
-      for (int sp = C::NSTG; sp < C::NSTG + kPrefetch; ++sp) prefetch(sp);
       for (int st = 0; st < nstg; ++st) {
-        if (kPrefetch > 0 && st >= C::NSTG) prefetch(st + kPrefetch);
         const int s = st % C::NSTG;
         sm100::mbar_wait(&stg_empty[s], ((st / C::NSTG) & 1) ^ 1);
         uint8_t* dst = smem + C::OFF_STG + s * C::STG_BYTES;
-#if TCEC_EXP & 4
-        sm100::mbar_arrive(&stg_full[s]);
-        (void)dst;
-#else
-        if ((TCEC_EXP & 48) && (st & 1)) {
-          sm100::mbar_arrive(&stg_full[s]);
-          continue;
-        }
         sm100::mbar_arrive_expect_tx(&stg_full[s], C::STG_BYTES);
         sm100::tma_load_2d(dst, &tmA, &stg_full[s], st * C::BK_STG, m_cta);
 #pragma unroll
         for (int b = 0; b < 4; ++b)
           sm100::tma_load_2d(dst + C::STG_A_BYTES + b * C::STG_B_BOX, &tmB, &stg_full[s],
                              n_cta + 32 * b, st * C::BK_STG);
-#endif
       }
     } else if (warp == 1 && lane == 0 && rank == 0) {
       // ===================== MMA issuer (leader CTA) =====================
@@ -378,6 +382,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
       constexpr uint32_t b_hi_w = (uint32_t(C::B_SBO) >> 4) | (1u << 14) | (C::B_LAYOUT << 29);
       constexpr uint32_t b_lbo_w = (uint32_t(C::B_LBO) >> 4) << 16;
       constexpr uint32_t kB = C::B_KSTEP_BYTES >> 4;
+      uint32_t git = 0;
       for (int kb = 0; kb < nop; ++kb) {
         const int o = kb % C::NOP;
         sm100::mbar_wait_cluster(&op_full[o], (kb / C::NOP) & 1);
@@ -387,44 +392,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
         const uint32_t alo = ahi + (C::OP_A_BYTES >> 4);
         const uint32_t bhi = (op + ((2 * C::OP_A_BYTES) >> 4)) | b_lbo_w;
         const uint32_t blo = bhi + (C::OP_B_BYTES >> 4);
-        const bool first_in_interval = (kb % de) == 0;
-        if (shp.mma_order == 1 && !(first_in_interval && kb > 0)) {
-          // P is free: per k-step dA*B_hi, then A_hi*dB and A_hi*B_hi with A_hi
-          // held in the MMA's A collector (read from shared memory once).  The
-          // dC order per k-step is the reference's (schemes.py:294-298).
-#pragma unroll
-          for (int ks = 0; ks < 4; ++ks) {
-            sm100::mma_pair_col<V == kTF32, 0>(tmem_dC, alo + 2 * ks, a_hi_w, bhi + kB * ks, b_hi_w,
-                                               idesc, (kb | ks) != 0);
-            sm100::mma_pair_col<V == kTF32, 1>(tmem_dC, ahi + 2 * ks, a_hi_w, blo + kB * ks, b_hi_w,
-                                               idesc, 1u);
-            sm100::mma_pair_col<V == kTF32, 3>(tmem_P, ahi + 2 * ks, a_hi_w, bhi + kB * ks, b_hi_w,
-                                               idesc, !(first_in_interval && ks == 0));
-          }
-          sm100::mma_commit_pair_mc(&op_empty[o], 0x3);
-          if ((kb % de) == de - 1 || kb == nop - 1) sm100::mma_commit_pair_mc(p_full, 0x3);
-          continue;
-        }
-        // correction terms first (reference order per k-step: dA*B then A*dB) so the
-        // drain of the previous P overlaps them (schemes.py:294-298)
-#pragma unroll
-        for (int ks = 0; ks < 4; ++ks) {
-          sm100::mma_pair_split<V == kTF32>(tmem_dC, alo + 2 * ks, a_hi_w, bhi + kB * ks, b_hi_w,
-                                            idesc, (kb | ks) != 0);
-          sm100::mma_pair_split<V == kTF32>(tmem_dC, ahi + 2 * ks, a_hi_w, blo + kB * ks, b_hi_w,
-                                            idesc, 1u);
-        }
-        if (first_in_interval && kb > 0) {
-          sm100::mbar_wait_cluster(p_empty, ((kb / de) - 1) & 1);
-          sm100::tc_fence_after();
-        }
-#pragma unroll
-        for (int ks = 0; ks < 4; ++ks) {
-          sm100::mma_pair_split<V == kTF32>(tmem_P, ahi + 2 * ks, a_hi_w, bhi + kB * ks, b_hi_w,
-                                            idesc, !(first_in_interval && ks == 0));
-        }
+        c3_stage(
+            kb * 4, 4 * nop, de, git, p_empty, p_full,
+            [&](int ks) {  // reference order per k-step: dA*B_hi, then A_hi*dB
+              sm100::mma_pair_split<V == kTF32>(tmem_dC, alo + 2 * ks, a_hi_w, bhi + kB * ks,
+                                                b_hi_w, idesc, (kb | ks) != 0);
+              sm100::mma_pair_split<V == kTF32>(tmem_dC, ahi + 2 * ks, a_hi_w, blo + kB * ks,
+                                                b_hi_w, idesc, 1u);
+            },
+            [&](int ks, uint32_t acc) {
+              sm100::mma_pair_split<V == kTF32>(tmem_P, ahi + 2 * ks, a_hi_w, bhi + kB * ks, b_hi_w,
+                                                idesc, acc);
+            });
         sm100::mma_commit_pair_mc(&op_empty[o], 0x3);
-        if ((kb % de) == de - 1 || kb == nop - 1) sm100::mma_commit_pair_mc(p_full, 0x3);
       }
     }
   } else if (warp < C::DRAIN_WARP0) {
@@ -459,7 +439,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
       sm100::mbar_wait(p_full, it & 1);
       sm100::tc_fence_after();
 #pragma unroll
-      for (int c = 0; c < ((TCEC_EXP & 2) ? 0 : 16); ++c) {
+      for (int c = 0; c < 16; ++c) {
         // 8 columns at a time: fewer live temporaries next to the 128 accumulators
         uint32_t r[8];
         sm100::tmem_ld_32x32b_x8(tmem_P + lane_off + h * 128 + c * 8, r);

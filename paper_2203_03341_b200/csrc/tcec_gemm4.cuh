@@ -233,7 +233,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
   const int n_cta = n_pair + rank * C::BN_CTA;
   const int nop = shp.num_op_stages;
   const int nstg = nop * VC::STG_PER_OP;
-  const int de = shp.drain_every;
+  const int de = shp.drain_every / 4;  // operand stages per drain interval (host: a multiple of 4 k-steps)
   const int nintervals = (nop + de - 1) / de;
 
   if (warp == 0 && lane == 0) {

@@ -105,7 +105,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
   const int npairs = gridDim.x >> 1;
   const int pid = blockIdx.x >> 1;
   const int nop = shp.num_op_stages;
-  const int de = shp.drain_every;
+  const int de = shp.drain_every;  // MMA k-steps per drain interval
   const int nparts = kSplitK ? ksplit : 1;
   const int num_units = num_tiles * nparts;
   // unit -> (tile, operand stages [kb0, kb1))
@@ -216,27 +216,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
           const uint32_t alo = ahi + (C::OP_A_BYTES >> 4);
           const uint32_t bhi = (op + ((2 * C::OP_A_BYTES) >> 4)) | b_lbo_w;
           const uint32_t blo = bhi + (C::OP_B_BYTES >> 4);
-#pragma unroll
-          for (int ks = 0; ks < 4; ++ks) {  // schemes.py:294-298
-            sm100::mma_pair_split<V == kTF32>(tmem_dC, alo + 2 * ks, a_hi_w, bhi + kB * ks, b_hi_w,
-                                              idesc, (kb | ks) != 0);
-            sm100::mma_pair_split<V == kTF32>(tmem_dC, ahi + 2 * ks, a_hi_w, blo + kB * ks, b_hi_w,
-                                              idesc, 1u);
-          }
-          const bool first_in_interval = (kb % de) == 0;
-          if (first_in_interval && git > 0) {
-            sm100::mbar_wait_cluster(p_empty, (git - 1) & 1);
-            sm100::tc_fence_after();
-          }
-#pragma unroll
-          for (int ks = 0; ks < 4; ++ks)
-            sm100::mma_pair_split<V == kTF32>(tmem_P, ahi + 2 * ks, a_hi_w, bhi + kB * ks, b_hi_w,
-                                              idesc, !(first_in_interval && ks == 0));
+          c3_stage(
+              kb * 4, 4 * nop_u, de, git, p_empty, p_full,
+              [&](int ks) {  // schemes.py:294-298: dA*B_hi, then A_hi*dB
+                sm100::mma_pair_split<V == kTF32>(tmem_dC, alo + 2 * ks, a_hi_w, bhi + kB * ks,
+                                                  b_hi_w, idesc, (kb | ks) != 0);
+                sm100::mma_pair_split<V == kTF32>(tmem_dC, ahi + 2 * ks, a_hi_w, blo + kB * ks,
+                                                  b_hi_w, idesc, 1u);
+              },
+              [&](int ks, uint32_t acc) {
+                sm100::mma_pair_split<V == kTF32>(tmem_P, ahi + 2 * ks, a_hi_w, bhi + kB * ks,
+                                                  b_hi_w, idesc, acc);
+              });
           sm100::mma_commit_pair_mc(&op_empty[o], 0x3);
-          if ((kb % de) == de - 1 || kb == nop_u - 1) {
-            sm100::mma_commit_pair_mc(p_full, 0x3);
-            ++git;
-          }
         }
       }
     }
@@ -277,7 +269,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
     for (int u = pid; u < num_units; u += npairs) {
       int tile, part, kb0, kb1;
       unit_of(u, tile, part, kb0, kb1);
-      const int nintervals = (kb1 - kb0 + de - 1) / de;
+      const int nintervals = (4 * (kb1 - kb0) + de - 1) / de;
       int tm, tn;
       grouped_tile(tile, tiles_m, tiles_n, shp.group_m, tm, tn);
       float acc[128];

@@ -239,10 +239,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PsCfg<V, S>::NUM_THR
   const int pid = blockIdx.x >> 1;
   const int nop = shp.num_op_stages;
   const int de = shp.drain_every;
-  // drain intervals per tile: op-stage groups (corrected3), blocks of `de` MMA
-  // k-steps (4 per op stage) for kSchIn4RN, else one (the epilogue)
-  const int nintervals = C::kDrain ? (nop + de - 1) / de
-                                   : (S == kSchIn4RN ? (4 * nop + de - 1) / de : 1);
+  // drain intervals per tile: blocks of `de` MMA k-steps (4 per op stage) for
+  // corrected3 and kSchIn4RN, else one (the epilogue)
+  const int nintervals = C::kDrain || S == kSchIn4RN ? (4 * nop + de - 1) / de : 1;
 
   if (warp == 0 && lane == 0) {
     if (smem_base & 1023u) __trap();
@@ -364,29 +363,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PsCfg<V, S>::NUM_THR
               sm100::mma_pair_split<V == kTF32>(tmem_P, ahi + 2 * ks, hi_w, bhi + 2 * ks, hi_w, idesc, 1u);
             }
           } else {
-            // corrections first (reference order per k-step: dA*B then A*dB), so the
-            // drain of the previous P overlaps them (schemes.py:294-298)
-#pragma unroll
-            for (int ks = 0; ks < 4; ++ks) {
-              sm100::mma_pair_split<V == kTF32>(tmem_dC, alo + 2 * ks, hi_w, bhi + 2 * ks, hi_w, idesc,
-                                                (kb | ks) != 0);
-              sm100::mma_pair_split<V == kTF32>(tmem_dC, ahi + 2 * ks, hi_w, blo + 2 * ks, hi_w, idesc, 1u);
-              if constexpr (S == kSchC3DD)  // schemes.py:308-313: the dA*dB chain
-                sm100::mma_pair_split<V == kTF32>(tmem_ddC, alo + 2 * ks, hi_w, blo + 2 * ks, hi_w,
-                                                  idesc, (kb | ks) != 0);
-            }
-            const bool first_in_interval = (kb % de) == 0;
-            if (first_in_interval && git > 0) {
-              sm100::mbar_wait_cluster(p_empty, (git - 1) & 1);
-              sm100::tc_fence_after();
-            }
-#pragma unroll
-            for (int ks = 0; ks < 4; ++ks)
-              sm100::mma_pair_split<V == kTF32>(tmem_P, ahi + 2 * ks, hi_w, bhi + 2 * ks, hi_w, idesc,
-                                                !(first_in_interval && ks == 0));
+            c3_stage(
+                kb * 4, 4 * nop, de, git, p_empty, p_full,
+                [&](int ks) {  // reference order per k-step: dA*B then A*dB (schemes.py:294-298)
+                  sm100::mma_pair_split<V == kTF32>(tmem_dC, alo + 2 * ks, hi_w, bhi + 2 * ks, hi_w,
+                                                    idesc, (kb | ks) != 0);
+                  sm100::mma_pair_split<V == kTF32>(tmem_dC, ahi + 2 * ks, hi_w, blo + 2 * ks, hi_w,
+                                                    idesc, 1u);
+                  if constexpr (S == kSchC3DD)  // schemes.py:308-313: the dA*dB chain
+                    sm100::mma_pair_split<V == kTF32>(tmem_ddC, alo + 2 * ks, hi_w, blo + 2 * ks,
+                                                      hi_w, idesc, (kb | ks) != 0);
+                },
+                [&](int ks, uint32_t acc) {
+                  sm100::mma_pair_split<V == kTF32>(tmem_P, ahi + 2 * ks, hi_w, bhi + 2 * ks, hi_w,
+                                                    idesc, acc);
+                });
           }
           sm100::mma_commit_pair_mc(&op_empty[o], 0x3);
-          if (S != kSchIn4RN && (kb == nop - 1 || (C::kDrain && (kb % de) == de - 1))) {
+          if ((S == kSchPlain || S == kSchIn4) && kb == nop - 1) {
             sm100::mma_commit_pair_mc(p_full, 0x3);
             ++git;
           }

@@ -131,8 +131,9 @@ class GemmRun:
 @dataclass(frozen=True)
 class MmaConfig:
     """mma.py:26-45.  On the GPU, block_k is the drain interval of the main-term
-    partial (rounded up to a whole operand stage: 64 for FP16, 32 for TF32); the
-    accumulator width is the hardware's and acc_significand_bits is not used."""
+    partial (schemes.py:300-304): any multiple of the MMA k-step (16 FP16, 8
+    TF32).  The accumulator inside one MMA is the tensor core's own, so
+    acc_significand_bits must keep the reference's default (25)."""
 
     input_format: FloatFormat = FP16
     acc_significand_bits: int = 25
@@ -155,28 +156,31 @@ def default_config(scheme, block_k: int = 16, acc_bits: int = 25) -> MmaConfig:
 
 
 STAGE_K = {N.TCEC_FP16: 64, N.TCEC_TF32: 32}
-# Default drain interval of the main-term partial: measured on B200 to be both
-# faster and more accurate against FP64 than one operand stage.
+# Default drain interval of the main-term partial when no MmaConfig is given:
+# measured on B200 to be both faster and more accurate against FP64 than the
+# reference's per-block drain.
 DEFAULT_DRAIN_K = {N.TCEC_FP16: 128, N.TCEC_TF32: 64}
-
 
 MMA_K = {N.TCEC_FP16: 16, N.TCEC_TF32: 8}
 
 
-def drain_k_for(variant: int, block_k: int, sched: int = 0) -> int:
-    """Drain interval the kernel uses for MmaConfig.block_k: the reference's
-    per-block drain (block_k = 16) is never more accurate on the hardware than
-    the default interval, so block_k selects max(default, block_k rounded up to
-    whole operand stages).  corrected4_rn (SCHED_INUNIT4_RN) drains every block
-    of every product, so there block_k is taken as is (a multiple of the MMA
-    k-step)."""
-    if sched == SCHED_INUNIT4_RN:
-        if int(block_k) % MMA_K[variant]:
-            raise NotImplementedError(
-                f"corrected4_rn on the tensor core needs block_k a multiple of {MMA_K[variant]}")
-        return int(block_k)
-    stage = STAGE_K[variant]
-    return max(DEFAULT_DRAIN_K[variant], stage * max(1, -(-int(block_k) // stage)))
+def drain_k_for(variant: int, cfg: MmaConfig | None, sched: int = 0) -> int:
+    """Drain interval the kernel uses (tcec_opts.drain_k).  cfg=None: the tuned
+    default (128 FP16 / 64 TF32; 16 for corrected4_rn, the reference's block).
+    An explicit MmaConfig: its block_k, the reference's drain schedule
+    (schemes.py:300-304, mma.py:34), which must be a whole number of MMA
+    k-steps (16 FP16, 8 TF32)."""
+    if cfg is None:
+        return 16 if sched == SCHED_INUNIT4_RN else DEFAULT_DRAIN_K[variant]
+    if getattr(cfg, "acc_significand_bits", 25) != 25:
+        raise NotImplementedError(
+            "the tensor core's accumulator is fixed; acc_significand_bits applies to the "
+            "reference's emulator only")
+    block_k = int(cfg.block_k)
+    if block_k % MMA_K[variant]:
+        raise NotImplementedError(
+            f"block_k={block_k} is not a multiple of the tensor core's k-step ({MMA_K[variant]})")
+    return block_k
 
 
 # Product schedules of the kernel (include/tcec.h TCEC_SCHEME_*).
@@ -257,6 +261,24 @@ def _as_fp32_host(a) -> np.ndarray:
     return x32
 
 
+def _as_fp32_device(t):
+    """schemes.py:163-171 for CUDA tensors of another dtype: the values must be
+    finite and exactly representable in FP32 (checked on the device, one
+    synchronisation); float32 tensors pass through (the kernel flags
+    non-finite inputs)."""
+    import torch
+
+    if t.dtype == torch.float32:
+        return t
+    x64 = t.to(torch.float64)
+    if not bool(torch.isfinite(x64).all()):
+        raise ValueError("gemm requires finite inputs")
+    x32 = x64.to(torch.float32)
+    if not torch.equal(x32.to(torch.float64), x64):
+        raise ValueError("inputs must hold FP32 values")
+    return x32
+
+
 def _flags_to_run(fl: int) -> RunFlags:
     if fl & N.FLAG_NONFINITE_INPUT:
         raise ValueError("gemm requires finite inputs")
@@ -279,10 +301,21 @@ def _tma_ready(t):
     return buf[:, :cols], ld
 
 
+def _check_out(out, m: int, n: int, device) -> None:
+    import torch
+
+    if not (_is_torch(out) and out.is_cuda and out.device == device):
+        raise ValueError("out must be a CUDA tensor on the operands' device")
+    if out.dtype != torch.float32 or out.dim() != 2 or tuple(out.shape) != (m, n):
+        raise ValueError(f"out must be a float32 tensor of shape ({m}, {n})")
+    if not (out.stride(1) == 1 and out.stride(0) % 4 == 0 and out.stride(0) >= max(n, 1)
+            and out.data_ptr() % 16 == 0):
+        raise ValueError("out must have unit inner stride and a 16-byte aligned leading dimension")
+
+
 def gemm_device(a, b, scheme="corrected3_halfhalf", cfg: MmaConfig | None = None, out=None,
-                flags=None, block_n: int = 0, group_m: int = 0, prefetch: int = 0,
-                kernel_variant: int = 0, drain_k: int | None = None, mma_order: int = 0,
-                split_mode: int = 0, split_k: int = 0):
+                flags=None, block_n: int = 0, group_m: int = 0, kernel_variant: int = 0,
+                drain_k: int | None = None, split_mode: int = 0, split_k: int = 0):
     """C = A @ B on CUDA float32 tensors, stream-ordered on torch's current stream.
 
     No host synchronisation: `flags` (int32 CUDA tensor, one element, caller
@@ -299,27 +332,28 @@ def gemm_device(a, b, scheme="corrected3_halfhalf", cfg: MmaConfig | None = None
         raise ValueError(f"inner dimensions differ: {k} vs {kb}")
     if a.dtype != torch.float32 or b.dtype != torch.float32:
         raise ValueError("inputs must hold FP32 values")
-    if not (a.is_cuda and b.is_cuda):
-        raise ValueError("gemm_device expects CUDA tensors")
+    if not (a.is_cuda and b.is_cuda) or a.device != b.device:
+        raise ValueError("gemm_device expects CUDA tensors on one device")
+    if flags is not None and not (_is_torch(flags) and flags.is_cuda and flags.device == a.device
+                                  and flags.dtype == torch.int32 and flags.numel() >= 1):
+        raise ValueError("flags must be an int32 CUDA tensor on the operands' device")
     if out is None:
         ldc = max(4, (n + 3) // 4 * 4)
         out = torch.empty((m, ldc), dtype=torch.float32, device=a.device)[:, :n]
+    else:
+        _check_out(out, m, n, a.device)
     if m == 0 or n == 0:
         return out
     if k == 0:  # zero blocks: C = 0 exactly (schemes.py:300-307)
         return out.zero_()
-    block_k = cfg.block_k if cfg is not None else 16
-    dk = drain_k if drain_k is not None else drain_k_for(variant, block_k, sched)
+    dk = drain_k if drain_k is not None else drain_k_for(variant, cfg, sched)
     opts = N.make_opts(split_rounding=rounding, scale_log2=scale,
                        drain_k=dk, block_n=block_n, group_m=group_m,
-                       prefetch=prefetch, kernel_variant=kernel_variant,
-                       mma_order=mma_order, split_mode=split_mode, scheme=sched,
+                       kernel_variant=kernel_variant, split_mode=split_mode, scheme=sched,
                        split_k=split_k)
     A, lda = _tma_ready(a)
     B, ldb = _tma_ready(b)
     C, ldc = out, out.stride(0)
-    if not (C.stride(1) == 1 and ldc % 4 == 0 and C.data_ptr() % 16 == 0):
-        raise ValueError("out must have unit inner stride and a 16-byte aligned leading dimension")
     stream = torch.cuda.current_stream(a.device).cuda_stream
     N.check(N.lib().tcec_sgemm(variant, m, n, k, A.data_ptr(), lda, B.data_ptr(), ldb,
                                C.data_ptr(), ldc, ctypes.byref(opts),
@@ -341,6 +375,8 @@ def gemm_device_multi(a, b, outs, scheme="corrected3_halfhalf", cfg: MmaConfig |
         raise ValueError("gemm expects 2-D matrices with matching inner dimensions")
     if a.dtype != torch.float32 or b.dtype != torch.float32:
         raise ValueError("inputs must hold FP32 values")
+    if not (a.is_cuda and b.is_cuda) or a.device != b.device:
+        raise ValueError("gemm_device_multi expects CUDA tensors on one device")
     outs = list(outs)
     if not 1 <= len(outs) <= 8:
         raise ValueError("1..8 destinations")
@@ -348,13 +384,14 @@ def gemm_device_multi(a, b, outs, scheme="corrected3_halfhalf", cfg: MmaConfig |
     n = b.shape[1]
     ldc = outs[0].stride(0)
     for o in outs:
-        if o.shape != (m, n) or o.stride(0) != ldc or o.stride(1) != 1 or o.dtype != torch.float32:
-            raise ValueError("destinations must be float32 (m, n) views with one leading dimension")
+        if not _is_torch(o) or not o.is_cuda or tuple(o.shape) != (m, n) or o.stride(0) != ldc \
+                or o.stride(1) != 1 or o.dtype != torch.float32 or o.data_ptr() % 16:
+            raise ValueError("destinations must be float32 CUDA (m, n) views with one "
+                             "16-byte aligned leading dimension")
     if ldc % 4:
         raise ValueError("destination leading dimension must be a multiple of 4")
-    block_k = cfg.block_k if cfg is not None else 16
     opts = N.make_opts(split_rounding=rounding, scale_log2=scale,
-                       drain_k=drain_k_for(variant, block_k))
+                       drain_k=drain_k_for(variant, cfg), kernel_variant=4)
     A, lda = _tma_ready(a)
     B, ldb = _tma_ready(b)
     ptrs = (ctypes.c_void_p * len(outs))(*[o.data_ptr() for o in outs])
@@ -378,7 +415,6 @@ def gemm(a, b, scheme, cfg: MmaConfig | None = None, out=None) -> GemmRun:
     device inputs.
     """
     variant, rounding, scale, sched = resolve_schedule(scheme)
-    block_k = cfg.block_k if cfg is not None else 16
     if _is_torch(a) and a.is_cuda:
         import torch
 
@@ -386,8 +422,8 @@ def gemm(a, b, scheme, cfg: MmaConfig | None = None, out=None) -> GemmRun:
             raise ValueError("both operands must live on the same kind of memory")
         if a.dim() != 2 or b.dim() != 2:
             raise ValueError("gemm expects 2-D matrices")
-        a32 = a if a.dtype == torch.float32 else a.to(torch.float32)
-        b32 = b if b.dtype == torch.float32 else b.to(torch.float32)
+        a32 = _as_fp32_device(a)
+        b32 = _as_fp32_device(b)
         fl = torch.zeros(1, dtype=torch.int32, device=a.device)
         out = gemm_device(a32, b32, scheme, cfg, out=out, flags=fl)
         m, k = a.shape
@@ -411,7 +447,7 @@ def gemm(a, b, scheme, cfg: MmaConfig | None = None, out=None) -> GemmRun:
         C = np.empty((m, n), dtype=np.float32)
     fl = ctypes.c_uint32(0)
     opts = N.make_opts(split_rounding=rounding, scale_log2=scale,
-                       drain_k=drain_k_for(variant, block_k, sched), scheme=sched)
+                       drain_k=drain_k_for(variant, cfg, sched), scheme=sched)
     N.check(N.lib().tcec_sgemm_host(variant, m, n, k, A.ctypes.data, max(k, 1), B.ctypes.data,
                                     max(n, 1), C.ctypes.data, max(n, 1), ctypes.byref(opts),
                                     ctypes.byref(fl), None), "tcec_sgemm_host")
@@ -441,13 +477,12 @@ def delta_term_ablation(a, b, split: SplitScheme | None = None, cfg: MmaConfig |
     kb, n = B.shape
     if kb != k:
         raise ValueError(f"inner dimensions differ: {k} vs {kb}")
-    block_k = cfg.block_k if cfg is not None else 16
     outs = []
     for sched in (SCHED_CORRECTED3, SCHED_CORRECTED3_DD):
         C = np.empty((m, n), dtype=np.float32)
         fl = ctypes.c_uint32(0)
         opts = N.make_opts(split_rounding=rounding, scale_log2=scale,
-                           drain_k=drain_k_for(variant, block_k), scheme=sched)
+                           drain_k=drain_k_for(variant, cfg), scheme=sched)
         N.check(N.lib().tcec_sgemm_host(variant, m, n, k, np.ascontiguousarray(A).ctypes.data,
                                         max(k, 1), np.ascontiguousarray(B).ctypes.data, max(n, 1),
                                         C.ctypes.data, max(n, 1), ctypes.byref(opts),

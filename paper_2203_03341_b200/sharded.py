@@ -27,9 +27,30 @@ def row_slab(m: int, rank: int, world: int) -> tuple[int, int]:
     return start, min(m, start + per)
 
 
+def _device_compute(flags, concurrent: bool) -> Callable:
+    """The sm_100a kernel, its RunFlags OR-ed into `flags` (device int32).  With
+    a collective in flight on another stream the per-tile kernel is pinned
+    (kernel_variant 4): the lock-step persistent kernel assumes it has every SM."""
+    from .schemes import gemm_device
+
+    def compute(a, bb, sch):
+        return gemm_device(a, bb, sch, flags=flags, kernel_variant=4 if concurrent else 0)
+
+    return compute
+
+
+def _raise_on_flags(flags) -> None:
+    """The reference raises ValueError for non-finite inputs (schemes.py:166-167);
+    numerical anomalies only set RunFlags."""
+    from . import _native as N
+
+    if int(flags.item()) & N.FLAG_NONFINITE_INPUT:
+        raise ValueError("gemm requires finite inputs")
+
+
 def sharded_gemm(a_slab, b, scheme="corrected3_halfhalf", *, m_total: Optional[int] = None,
                  allgather: bool = False, group=None, out=None,
-                 compute: Optional[Callable] = None, overlap_chunks: int = 1):
+                 compute: Optional[Callable] = None, overlap_chunks: int = 1, flags=None):
     """C_slab = A_slab @ B on this rank; optionally all-gather the full C.
 
     a_slab: this rank's rows of A (rows row_slab(m_total, rank, world)), b: the
@@ -37,6 +58,11 @@ def sharded_gemm(a_slab, b, scheme="corrected3_halfhalf", *, m_total: Optional[i
     `allgather`.  `compute(a, b, scheme)` defaults to the sm_100a kernel
     (gemm_device); tests may substitute the CPU oracle to exercise the
     partition / gather logic on gloo without a GPU.
+
+    RunFlags: with `flags` (int32 CUDA tensor, caller-zeroed) the kernel ORs
+    this rank's TCEC_FLAG_* bits into it and nothing synchronises; without it
+    the call reads them once at the end and raises ValueError for non-finite
+    inputs in this rank's operands, as the reference does.
 
     overlap_chunks > 1 (with allgather): the slab is computed in that many row
     chunks (multiples of the 256-row pair tile) and chunk i is all-gathered on
@@ -49,16 +75,21 @@ def sharded_gemm(a_slab, b, scheme="corrected3_halfhalf", *, m_total: Optional[i
 
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
+    own_flags = None
     if compute is None:
-        from .schemes import gemm_device
-
-        def compute(a, bb, sch):
-            return gemm_device(a, bb, sch)
+        if flags is None:
+            flags = own_flags = torch.zeros(1, dtype=torch.int32, device=b.device)
+        compute = _device_compute(flags, allgather and world > 1 and overlap_chunks > 1)
 
     if allgather and world > 1 and overlap_chunks > 1:
-        return _gather_overlapped(a_slab, b, scheme, m_total, world, group, out, compute,
-                                  overlap_chunks)
+        result = _gather_overlapped(a_slab, b, scheme, m_total, world, group, out, compute,
+                                    overlap_chunks)
+        if own_flags is not None:
+            _raise_on_flags(own_flags)
+        return result
     c_slab = compute(a_slab, b, scheme)
+    if own_flags is not None:
+        _raise_on_flags(own_flags)
     if not allgather or world == 1:
         return c_slab
     if m_total is None:
@@ -128,7 +159,8 @@ def _gather_overlapped(a_slab, b, scheme, m_total, world, group, out, compute, c
 _SYMM_CACHE: dict = {}
 
 
-def sharded_gemm_fused(a_slab, b, scheme="corrected3_halfhalf", *, m_total: int, group=None):
+def sharded_gemm_fused(a_slab, b, scheme="corrected3_halfhalf", *, m_total: int, group=None,
+                       copy: bool = True, flags=None):
     """Row-sharded GEMM with the all-gather fused into the GEMM epilogue.
 
     The full C lives in symmetric memory (torch.distributed._symmetric_memory:
@@ -138,6 +170,12 @@ def sharded_gemm_fused(a_slab, b, scheme="corrected3_halfhalf", *, m_total: int,
     buffer, so the gather overlaps the GEMM tile by tile with no separate
     collective; a barrier then makes the peers' stores visible.  Returns this
     rank's full (m_total x n) C.  Bit-identical to the single-GPU product.
+
+    The symmetric buffer is cached per shape and reused: a barrier before the
+    GEMM makes every rank finish with the previous call's result before any
+    peer overwrites it, and the result is returned as a copy (copy=False
+    returns a view of the buffer, valid until the next call with this shape).
+    RunFlags as in sharded_gemm.
     """
     import torch
     import torch.distributed as dist
@@ -163,7 +201,14 @@ def sharded_gemm_fused(a_slab, b, scheme="corrected3_halfhalf", *, m_total: int,
     # own buffer first, then the peers'
     order = [rank] + [r for r in range(world) if r != rank]
     outs = [hdl.get_buffer(r, (per * world, ldc), torch.float32)[r0:r0 + rows, :n] for r in order]
+    own_flags = None
+    if flags is None:
+        flags = own_flags = torch.zeros(1, dtype=torch.int32, device=b.device)
+    hdl.barrier()  # every rank is done with the previous result in this buffer
     if rows > 0:
-        gemm_device_multi(a_slab, b, outs, scheme)
-    hdl.barrier()
-    return full[:m_total, :n]
+        gemm_device_multi(a_slab, b, outs, scheme, flags=flags)
+    hdl.barrier()  # the peers' stores into this rank's buffer are complete
+    if own_flags is not None:
+        _raise_on_flags(own_flags)
+    result = full[:m_total, :n]
+    return result.clone() if copy else result

@@ -223,26 +223,26 @@ def test_row_and_column_separable(sname, variant, bk, drain):
 
 @pytest.mark.parametrize("sname,variant,bk,drain", VARIANTS)
 def test_drain_interval_option(sname, variant, bk, drain):
-    """Every supported drain interval (whole operand stages) matches the oracle's
-    drain restatement at that interval; MmaConfig.block_k maps to
-    max(default, block_k rounded up to stages)."""
+    """Every drain interval -- any whole number of MMA k-steps, including the
+    reference's block_k = 16 and intervals that straddle operand stages --
+    matches the oracle's drain restatement at that interval; an explicit
+    MmaConfig.block_k selects exactly that drain."""
     import torch
 
     T = _T()
-    a = O.urand(128, 1024, -1, 1, 9)
-    b = O.urand(1024, 128, -1, 1, O.pair_seed(9))
-    stage = 64 if variant == "fp16" else 32
+    a = O.urand(128, 1000, -1, 1, 9)
+    b = O.urand(1000, 136, -1, 1, O.pair_seed(9))
     A, B = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
-    for d in (stage, 2 * stage, 4 * stage, 8 * stage):
+    for d in (bk, 2 * bk, 3 * bk, 4 * bk, 5 * bk, 8 * bk, 32 * bk):
         c = T.gemm_device(A, B, sname, drain_k=d).cpu().numpy()
         oc, _ = O.corrected3(a, b, variant, block_k=bk, drain_k=d)
         _check_close(c, oc, a, b, (sname, d), variant)
-    v = 0 if variant == "fp16" else 1
-    assert T.schemes.drain_k_for(v, 16) == drain
-    assert T.schemes.drain_k_for(v, 4 * drain) == 4 * drain
-    c_cfg, _ = _run(a, b, sname, cfg=T.MmaConfig(block_k=4 * drain))
-    c_dk = T.gemm_device(A, B, sname, drain_k=4 * drain).cpu().numpy()
-    assert np.array_equal(c_cfg, c_dk)
+    for d in (16, 48, 4 * drain):
+        c_cfg, _ = _run(a, b, sname, cfg=T.MmaConfig(block_k=d))
+        c_dk = T.gemm_device(A, B, sname, drain_k=d).cpu().numpy()
+        assert np.array_equal(c_cfg, c_dk), d
+    c_def, _ = _run(a, b, sname)
+    assert np.array_equal(c_def, T.gemm_device(A, B, sname, drain_k=drain).cpu().numpy())
 
 
 @pytest.mark.parametrize("shape", [(130, 61, 77), (1100, 700, 300)])
@@ -383,30 +383,9 @@ def test_pair_kernel_bitwise_equals_single_cta_kernel(sname, variant, bk, drain,
     assert int(f1.item()) == int(f2.item()) == int(f3.item())
 
 
-@pytest.mark.parametrize("kv", [1])
-@pytest.mark.parametrize("sname,variant,bk,drain", VARIANTS)
-def test_kernel_variants_bitwise_equal(sname, variant, bk, drain, kv):
-    """The pair-kernel variants (1: unified split+drain workers, 2: FP32 loaded
-    straight to registers, no staging ring) run the same per-element arithmetic
-    as the staged pair kernel: bit-identical outputs and flags, including ragged
-    edges."""
-    import torch
-
-    T = _T()
-    g = torch.Generator(device="cuda")
-    g.manual_seed(11)
-    A = torch.rand((520, 1004), generator=g, device="cuda") * 2 - 1
-    B = torch.rand((1004, 300), generator=g, device="cuda") * 2 - 1
-    f0 = torch.zeros(1, dtype=torch.int32, device="cuda")
-    f1 = torch.zeros(1, dtype=torch.int32, device="cuda")
-    c0 = T.gemm_device(A, B, sname, flags=f0)
-    c1 = T.gemm_device(A, B, sname, flags=f1, kernel_variant=kv)
-    assert torch.equal(c0.view(torch.int32), c1.view(torch.int32))
-    assert int(f0.item()) == int(f1.item())
-
-
-OPTION_SETS = [{"block_n": 128}, {"block_n": 128, "kernel_variant": 1}, {"block_n": 192}, {"block_n": 256}, {"kernel_variant": 5}, {"mma_order": 1}, {"split_mode": 2}, {"kernel_variant": 2},
-               {"kernel_variant": 3}, {"kernel_variant": 4}]
+OPTION_SETS = [{"block_n": 128}, {"block_n": 128, "kernel_variant": 1}, {"block_n": 192},
+               {"block_n": 256}, {"split_mode": 2}, {"kernel_variant": 2}, {"kernel_variant": 3},
+               {"kernel_variant": 4}]
 
 
 @pytest.mark.parametrize("opts", OPTION_SETS, ids=lambda o: ",".join(f"{k}={v}" for k, v in o.items()))
@@ -414,9 +393,10 @@ OPTION_SETS = [{"block_n": 128}, {"block_n": 128, "kernel_variant": 1}, {"block_
 @pytest.mark.parametrize("shape", [(256, 192, 64), (300, 200, 1000), (77, 1000, 130), (520, 576, 2048)])
 def test_kernel_options_bitwise_equal(sname, variant, bk, drain, shape, opts):
     """Every kernel option runs the default path's per-element arithmetic: the
-    A-from-TMEM pair kernel (block_n=192), the A_hi collector-reuse MMA order
-    (mma_order=1) and the split-once mode (split_mode=2: separate split pass +
-    three-product GEMM over pre-split operands) give bit-identical C and flags,
+    A-from-TMEM pair kernels (block_n=192 / 128), the single-CTA kernel, the
+    persistent / lock-step / per-tile pair kernels and the split-once mode
+    (split_mode=2: separate split pass + three-product GEMM over pre-split
+    operands) give bit-identical C and flags,
     including ragged edges and inputs spanning 2^-40..2^15 (out_of_range for
     FP16; no hi overflow -- see test_split_once_mode_flags_and_overflow)."""
     import torch

@@ -67,11 +67,21 @@ def test_argument_validation_without_gpu(lib):
     # unsupported option combinations
     o = N.make_opts(split_rounding=N.ROUND_RN, scale_log2=5)
     assert f(0, 4, 4, 4, None, 4, None, 4, None, 4, ctypes.byref(o), None, None) == N.ERR_UNSUPPORTED
-    o = N.make_opts(drain_k=48)
+    # drain intervals are whole MMA k-steps (16 FP16, 8 TF32)
+    o = N.make_opts(drain_k=40)
+    assert f(0, 4, 4, 4, None, 4, None, 4, None, 4, ctypes.byref(o), None, None) == N.ERR_UNSUPPORTED
+    o = N.make_opts(drain_k=12)
+    assert f(1, 4, 4, 4, None, 4, None, 4, None, 4, ctypes.byref(o), None, None) == N.ERR_UNSUPPORTED
+    o = N.make_opts(drain_k=-16)
+    assert f(0, 4, 4, 4, None, 4, None, 4, None, 4, ctypes.byref(o), None, None) == N.ERR_UNSUPPORTED
+    # the narrow tiles drain whole operand stages; the single-CTA kernel is block_n 128 only
+    o = N.make_opts(drain_k=16, block_n=192)
+    assert f(0, 4, 4, 4, None, 4, None, 4, None, 4, ctypes.byref(o), None, None) == N.ERR_UNSUPPORTED
+    o = N.make_opts(kernel_variant=1)
     assert f(0, 4, 4, 4, None, 4, None, 4, None, 4, ctypes.byref(o), None, None) == N.ERR_UNSUPPORTED
     o = N.make_opts(scale_log2=11)
     assert f(1, 4, 4, 4, None, 4, None, 4, None, 4, ctypes.byref(o), None, None) == N.ERR_UNSUPPORTED
-    # corrected4_rn blocks are whole MMA k-steps; split_k in 0..64; kernel variants 0..5
+    # corrected4_rn blocks are whole MMA k-steps; split_k in 0..64; kernel variants 0..4
     o = N.make_opts(scheme=4, drain_k=24)
     assert f(0, 4, 4, 4, None, 4, None, 4, None, 4, ctypes.byref(o), None, None) == N.ERR_UNSUPPORTED
     o = N.make_opts(scheme=4, drain_k=12)
@@ -80,7 +90,7 @@ def test_argument_validation_without_gpu(lib):
     assert f(0, 4, 4, 4, None, 4, None, 4, None, 4, ctypes.byref(o), None, None) == N.ERR_UNSUPPORTED
     o = N.make_opts(split_k=65)
     assert f(0, 4, 4, 4, None, 4, None, 4, None, 4, ctypes.byref(o), None, None) == N.ERR_UNSUPPORTED
-    o = N.make_opts(kernel_variant=6)
+    o = N.make_opts(kernel_variant=5)
     assert f(0, 4, 4, 4, None, 4, None, 4, None, 4, ctypes.byref(o), None, None) == N.ERR_UNSUPPORTED
     o = N.make_opts(scheme=5)
     assert f(0, 4, 4, 4, None, 4, None, 4, None, 4, ctypes.byref(o), None, None) == N.ERR_UNSUPPORTED
@@ -169,13 +179,21 @@ def test_scheme_routing_without_gpu():
     rn_tf32 = T.corrected4(T.RoundingMode.RN, T.tf32tf32())
     assert T.resolve_schedule(rn_tf32) == (N.TCEC_TF32, N.ROUND_RNA, 0, S.SCHED_INUNIT4_RN)
     assert T.resolve_schedule("tc_plain_fp16")[3] == S.SCHED_TC_PLAIN
-    # corrected3 drains at least the default interval in whole stages; corrected4_rn
-    # drains exactly block_k (whole MMA k-steps)
-    assert S.drain_k_for(N.TCEC_FP16, 16) == 128 and S.drain_k_for(N.TCEC_TF32, 16) == 64
-    assert S.drain_k_for(N.TCEC_FP16, 16, S.SCHED_INUNIT4_RN) == 16
-    assert S.drain_k_for(N.TCEC_TF32, 8, S.SCHED_INUNIT4_RN) == 8
+    # no MmaConfig: the tuned default drain (corrected4_rn: the reference's block of
+    # 16); an explicit MmaConfig: exactly its block_k, in whole MMA k-steps
+    assert S.drain_k_for(N.TCEC_FP16, None) == 128 and S.drain_k_for(N.TCEC_TF32, None) == 64
+    assert S.drain_k_for(N.TCEC_FP16, None, S.SCHED_INUNIT4_RN) == 16
+    assert S.drain_k_for(N.TCEC_TF32, None, S.SCHED_INUNIT4_RN) == 16
+    assert S.drain_k_for(N.TCEC_FP16, S.MmaConfig(block_k=16)) == 16
+    assert S.drain_k_for(N.TCEC_TF32, S.MmaConfig(block_k=16)) == 16
+    assert S.drain_k_for(N.TCEC_TF32, S.MmaConfig(block_k=8)) == 8
+    assert S.drain_k_for(N.TCEC_FP16, S.default_config(T.SCHEMES_BY_NAME["corrected3_halfhalf"])) == 16
     with pytest.raises(NotImplementedError):
-        S.drain_k_for(N.TCEC_FP16, 24, S.SCHED_INUNIT4_RN)
+        S.drain_k_for(N.TCEC_FP16, S.MmaConfig(block_k=24))
+    with pytest.raises(NotImplementedError):
+        S.drain_k_for(N.TCEC_TF32, S.MmaConfig(block_k=12), S.SCHED_INUNIT4_RN)
+    with pytest.raises(NotImplementedError):  # the emulator's accumulator width has no GPU form
+        S.drain_k_for(N.TCEC_FP16, S.MmaConfig(block_k=16, acc_significand_bits=24))
     for name in ("fp64_ref", "fp32_simt", "fp32_lsbtrunc"):
         with pytest.raises(NotImplementedError):
             T.resolve_schedule(name)
