@@ -58,6 +58,9 @@ def lib():
         L.tcec_oracle_inunit.argtypes = [
             i32, i32, i32, i32, i32, i64, i64, i64, p, i64, p, i64, p, i64, i32, i32, p,
         ]
+        L.tcec_oracle_hw.argtypes = [
+            i32, i32, i32, i32, i64, i64, i64, p, i64, p, i64, p, i64, i32, i32, p,
+        ]
         L.tcec_oracle_fp32_simt.argtypes = [i64, i64, i64, p, i64, p, i64, p, i64, i32]
         L.tcec_oracle_fp64_ref.argtypes = [i64, i64, i64, p, i64, p, i64, p, i64]
         _lib = L
@@ -117,6 +120,60 @@ def corrected3(a, b, variant: str = "fp16", block_k: int = 16, drain_k: int | No
     if rc != 0:
         raise ValueError(f"oracle rejected arguments (rc={rc})")
     return c, int(flags.value)
+
+
+# MMA k-step (products per tcgen05.mma instruction) and the kernels' default
+# drain interval in k, per variant
+MMA_K = {"fp16": 16, "fp16u": 16, "tf32": 8}
+DEFAULT_DRAIN_K = {"fp16": 128, "fp16u": 128, "tf32": 64}
+
+
+def _hw(sched: int, a, b, fmt: int, s: int, rm: int, drain_ksteps: int, nthreads: int):
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    b = np.ascontiguousarray(b, dtype=np.float32)
+    m, k = a.shape
+    k2, n = b.shape
+    if k2 != k:
+        raise ValueError(f"inner dimensions differ: {k} vs {k2}")
+    c = np.empty((m, n), np.float32)
+    flags = ctypes.c_uint32(0)
+    rc = lib().tcec_oracle_hw(sched, fmt, s, rm, m, n, k, _ptr(a), k, _ptr(b), n, _ptr(c), n,
+                              drain_ksteps, nthreads, ctypes.byref(flags))
+    if rc != 0:
+        raise ValueError(f"oracle rejected arguments (rc={rc})")
+    return c, int(flags.value)
+
+
+def corrected3_hw(a, b, variant: str = "fp16", drain_k: int | None = None,
+                  include_dd: bool = False, rounding: int | None = None, nthreads: int = 0):
+    """The GPU kernels' corrected3 (tcec_oracle_hw): the reference's split and
+    product order with the B200 tensor core's measured MMA arithmetic and the
+    kernels' drain schedule (drain_k in k, a multiple of the MMA k-step;
+    default the kernels' 128 FP16 / 64 TF32).  Returns (C float32, flags int);
+    the GPU must match it bit for bit."""
+    fmt, s, rm = VARIANTS[variant]
+    if rounding is not None:
+        rm = rounding
+    d = drain_k or DEFAULT_DRAIN_K[variant]
+    if d % MMA_K[variant]:
+        raise ValueError("drain_k must be a multiple of the MMA k-step")
+    return _hw(1 if include_dd else 0, a, b, fmt, s, rm, d // MMA_K[variant], nthreads)
+
+
+def inunit_hw(a, b, scheme: str, block_k: int = 16, nthreads: int = 0):
+    """The GPU kernels' in-unit comparator schedules with the hardware MMA model
+    (tcec_oracle_hw): tc_plain_fp16 / tc_plain_tf32, markidis4 / markidis4_tf32
+    / corrected4_rz (one accumulator), corrected4_rn / corrected4_rn_tf32 (a
+    block of block_k per product, RN folds).  Returns (C float32, flags int)."""
+    kinds = {"tc_plain_fp16": (2, FMT_FP16, RM_RN), "tc_plain_tf32": (2, FMT_TF32, RM_RNA),
+             "markidis4": (3, FMT_FP16, RM_RN), "markidis4_tf32": (3, FMT_TF32, RM_RNA),
+             "corrected4_rz": (3, FMT_FP16, RM_RN), "corrected4_rn": (4, FMT_FP16, RM_RN),
+             "corrected4_rn_tf32": (4, FMT_TF32, RM_RNA)}
+    sched, fmt, rm = kinds[scheme]
+    kstep = 16 if fmt == FMT_FP16 else 8
+    if block_k % kstep:
+        raise ValueError("block_k must be a multiple of the MMA k-step")
+    return _hw(sched, a, b, fmt, 0, rm, block_k // kstep, nthreads)
 
 
 def inunit(a, b, scheme: str, block_k: int = 16, acc_bits: int = 25):

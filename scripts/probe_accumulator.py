@@ -143,5 +143,90 @@ def run_sets():
     print("saved", OUT)
 
 
+def run_edge_sets():
+    """Second round: the edges the random sets do not reach -- FP32-subnormal
+    and overflowing sums (TF32), non-finite operands (the FP16 hi of an input
+    >= 65520 is inf), negative zeros -- and corrected3 outputs of the full
+    kernels for offline comparison with the oracle's hardware mode."""
+    import torch
+
+    import paper_2203_03341_b200 as T
+
+    rng = np.random.default_rng(77)
+    sets = {}
+
+    def save(name, a, b, c):
+        sets[name + "__A"], sets[name + "__B"], sets[name + "__C"] = a, b, c
+        print(name, a.shape, b.shape, flush=True)
+
+    def plain(name, a, b, scheme):
+        A = torch.from_numpy(np.ascontiguousarray(a)).cuda()
+        B = torch.from_numpy(np.ascontiguousarray(b)).cuda()
+        save(name, a, b, T.gemm_device(A, B, scheme).cpu().numpy())
+
+    M = N = 256
+    # TF32 products landing in the FP32 subnormal range and around the overflow threshold
+    for k in (8, 32):
+        plain(f"tf32_subout_k{k}", tf32_values(rng, (M, k), -80, -60), tf32_values(rng, (k, N), -80, -60),
+              "tc_plain_tf32")
+        plain(f"tf32_ovf_k{k}", tf32_values(rng, (M, k), 60, 66), tf32_values(rng, (k, N), 60, 66),
+              "tc_plain_tf32")
+        # an accumulator in the subnormal range: a large-ish first instruction cancelled later
+        a = tf32_values(rng, (M, k), -75, -62)
+        b = tf32_values(rng, (k, N), -75, -62)
+        plain(f"tf32_subacc_k{k}", a, b, "tc_plain_tf32")
+    # non-finite operands: FP16 inf (as an operand value) and zeros, both signs
+    for fmt, scheme, big in (("f16", "tc_plain_fp16", np.float32(np.inf)),
+                             ("tf32", "tc_plain_tf32", np.float32(np.inf))):
+        k = 16 if fmt == "f16" else 8
+        vals = fp16_values if fmt == "f16" else tf32_values
+        a = vals(rng, (M, k), -4, 4)
+        b = vals(rng, (k, N), -4, 4)
+        mask = rng.random((M, k)) < 0.05
+        a[mask] = big * np.where(rng.random(mask.sum()) < 0.5, -1, 1)
+        zmask = rng.random((k, N)) < 0.2
+        b[zmask] = np.where(rng.random(zmask.sum()) < 0.5, -0.0, 0.0)
+        plain(f"{fmt}_inf_k{k}", a, b, scheme)
+        # signed zeros only
+        a = np.where(rng.random((M, k)) < 0.5, -0.0, 0.0).astype(np.float32)
+        a[:, 0] = vals(rng, (M, 1), -2, 2)[:, 0]
+        b = np.where(rng.random((k, N)) < 0.5, -0.0, 0.0).astype(np.float32)
+        plain(f"{fmt}_zeros_k{k}", a, b, scheme)
+    # corrected3 through the production kernels (default, reference drain, persistent)
+    for sname, tag in (("corrected3_halfhalf", "c3f16"), ("corrected3_tf32", "c3tf32")):
+        for dist, (lo, hi) in {"urand": (None, None), "exp": (-15, 14), "wide": (-40, 15)}.items():
+            m, n, k = 256, 256, 1000
+            if lo is None:
+                a = rng.uniform(-1, 1, (m, k)).astype(np.float32)
+                b = rng.uniform(-1, 1, (k, n)).astype(np.float32)
+            else:
+                a = (rng.uniform(1, 2, (m, k)) * np.exp2(rng.integers(lo, hi + 1, (m, k)))
+                     * rng.choice([-1, 1], (m, k))).astype(np.float32)
+                b = (rng.uniform(1, 2, (k, n)) * np.exp2(rng.integers(lo, hi + 1, (k, n)))
+                     * rng.choice([-1, 1], (k, n))).astype(np.float32)
+            A = torch.from_numpy(a).cuda()
+            B = torch.from_numpy(b).cuda()
+            for d in (0, 16, 48):
+                if d and "tf32" in sname:
+                    d //= 2
+                c = T.gemm_device(A, B, sname, drain_k=d or None).cpu().numpy()
+                save(f"{tag}_{dist}_d{d}", a, b, c)
+        # overflow: a few inputs at / above the FP16 hi threshold
+        a = rng.uniform(-1, 1, (256, 256)).astype(np.float32)
+        b = rng.uniform(-1, 1, (256, 256)).astype(np.float32)
+        a[3, 7] = 70000.0
+        a[5, :3] = [65520.0, -65536.0, 1e5]
+        b[9, 11] = -1e6
+        A = torch.from_numpy(a).cuda()
+        B = torch.from_numpy(b).cuda()
+        save(f"{tag}_ovf", a, b, T.gemm_device(A, B, sname).cpu().numpy())
+    out = os.path.join(ROOT, "gpurun_out", "probe_acc2.npz")
+    np.savez_compressed(out, **sets)
+    print("saved", out)
+
+
 if __name__ == "__main__":
-    run_sets()
+    if len(sys.argv) > 1 and sys.argv[1] == "edges":
+        run_edge_sets()
+    else:
+        run_sets()

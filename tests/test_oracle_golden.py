@@ -149,3 +149,65 @@ def test_inunit_comparators_match_reference_goldens():
             _same(c, g[f"{tag}__{sname}__C"])
             ov, oor = g[f"{tag}__{sname}__flags"]
             assert (bool(fl & 1), bool(fl & 2)) == (bool(ov), bool(oor)), (tag, sname, fl)
+
+
+# ---------------------------------------------------------------------------
+# The oracle's HARDWARE model (tcec_oracle_hw) against outputs recorded on the
+# B200: tests/golden/hw_probe_golden.npz (tests/golden/make_hw_fixture.py, from
+# scripts/probe_accumulator.py).  tc_plain datasets are raw tensor-core
+# accumulations (one instruction and chains, crafted / random / subnormal /
+# overflowing / non-finite operands); c3* datasets are the corrected3
+# kernels' outputs at the default and the reference's drain intervals.
+
+
+@pytest.fixture(scope="module")
+def hw_gold():
+    return np.load(os.path.join(GOLD, "hw_probe_golden.npz"))
+
+
+def _hw_cases(g):
+    return sorted({k.split("__")[0] for k in g.files})
+
+
+def test_hw_model_reproduces_tensor_core_outputs(hw_gold):
+    n = 0
+    for nm in _hw_cases(hw_gold):
+        a, b, c = hw_gold[nm + "__A"], hw_gold[nm + "__B"], hw_gold[nm + "__C"]
+        if nm.startswith("c3"):
+            continue
+        scheme = "tc_plain_fp16" if nm.startswith("f16") else "tc_plain_tf32"
+        oc, _ = O.inunit_hw(a, b, scheme)
+        _same(oc, c)
+        n += c.size
+    assert n > 15000
+
+
+def test_hw_model_reproduces_corrected3_kernel_outputs(hw_gold):
+    for nm in _hw_cases(hw_gold):
+        if not nm.startswith("c3"):
+            continue
+        variant = "fp16" if nm.startswith("c3f16") else "tf32"
+        drain = int(nm.split("_d")[1]) if "_d" in nm else 0
+        oc, _ = O.corrected3_hw(hw_gold[nm + "__A"], hw_gold[nm + "__B"], variant,
+                                drain_k=drain or None)
+        _same(oc, hw_gold[nm + "__C"])
+
+
+def test_hw_model_nonfinite_outputs_match_reference(gemm_gold):
+    """Where the reference's output is non-finite (hi overflow), the hardware
+    model gives the same value: +-inf with the same sign, or NaN."""
+    seen = 0
+    for tag in _cases(gemm_gold):
+        a, b = gemm_gold[f"{tag}__A"], gemm_gold[f"{tag}__B"]
+        for sname, variant in (("corrected3_halfhalf", "fp16"), ("corrected3_tf32", "tf32")):
+            ref = gemm_gold[f"{tag}__{sname}__C"]
+            bad = ~np.isfinite(ref)
+            if not bad.any():
+                continue
+            oc, fl = O.corrected3_hw(a, b, variant)
+            _same(oc[bad], ref[bad])
+            assert np.array_equal(np.isfinite(oc), ~bad)
+            ov, oor = gemm_gold[f"{tag}__{sname}__flags"]
+            assert (bool(fl & 1), bool(fl & 2)) == (bool(ov), bool(oor))
+            seen += int(bad.sum())
+    assert seen > 0
