@@ -160,6 +160,39 @@ def corrected3_hw(a, b, variant: str = "fp16", drain_k: int | None = None,
     return _hw(1 if include_dd else 0, a, b, fmt, s, rm, d // MMA_K[variant], nthreads)
 
 
+def corrected3_hw_split_k(a, b, variant: str, parts: int, drain_k: int | None = None,
+                          nthreads: int = 0):
+    """The split-K path (opts.split_k) with the hardware model: k in `parts`
+    contiguous ranges of whole operand stages (part p: stages
+    [p nop / S, (p + 1) nop / S), as tcec_gemm_pers_kernel<kSplitK> walks
+    them), each part's main-term sum and raw dC from the hardware model, then
+    tcec_splitk_reduce_kernel's fixed-order combine: c = RN(..RN(c_0 + c_1)..),
+    d likewise, C = RN(c + d 2^-s).  Returns (C float32, flags int)."""
+    fmt, s, rm = VARIANTS[variant]
+    d = drain_k or DEFAULT_DRAIN_K[variant]
+    de = d // MMA_K[variant]
+    stage = 64 if fmt == FMT_FP16 else 32
+    k = a.shape[1]
+    nop = -(-k // stage)
+    parts = min(parts, nop)
+    c = dc = None
+    flags = 0
+    for p in range(parts):
+        k0 = min(k, p * nop // parts * stage)
+        k1 = min(k, (p + 1) * nop // parts * stage)
+        cp, f1 = _hw(5, a[:, k0:k1], b[k0:k1], fmt, s, rm, de, nthreads)
+        dp, _ = _hw(6, a[:, k0:k1], b[k0:k1], fmt, s, rm, de, nthreads)
+        flags |= f1
+        c = cp if c is None else (c + cp).astype(np.float32)
+        dc = dp if dc is None else (dc + dp).astype(np.float32)
+    with np.errstate(all="ignore"):
+        # RN(c + dC 2^-s): the float64 sum is exact or far below FP32's half-ulp
+        out = (c.astype(np.float64) + dc.astype(np.float64) * 2.0 ** -s).astype(np.float32)
+    if not np.all(np.isfinite(out)):
+        flags |= FLAG_OVERFLOW
+    return out, flags
+
+
 def inunit_hw(a, b, scheme: str, block_k: int = 16, nthreads: int = 0):
     """The GPU kernels' in-unit comparator schedules with the hardware MMA model
     (tcec_oracle_hw): tc_plain_fp16 / tc_plain_tf32, markidis4 / markidis4_tf32

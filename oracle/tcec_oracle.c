@@ -281,7 +281,8 @@ typedef struct {
   int nonfinite_out;
 } hwjob_t;
 
-enum { HW_C3 = 0, HW_C3DD = 1, HW_PLAIN = 2, HW_IN4 = 3, HW_IN4RN = 4 };
+enum { HW_C3 = 0, HW_C3DD = 1, HW_PLAIN = 2, HW_IN4 = 3, HW_IN4RN = 4, HW_C3_MAIN = 5,
+       HW_C3_DC = 6 };
 
 /* The kernels' schedules (paper_2203_03341_b200/csrc: c3_stage in
  * tcec_gemm2.cuh, tcec_presplit.cuh) per output element, over k-steps j of the
@@ -294,7 +295,9 @@ enum { HW_C3 = 0, HW_C3DD = 1, HW_PLAIN = 2, HW_IN4 = 3, HW_IN4RN = 4 };
  *   PLAIN: P <- A_j B_j over all k (schemes.py:343-351)
  *   IN4:   P <- dA dB, dA B, A dB, A B per k-step, one accumulator (:352-364)
  *   IN4RN: the same four, each in its own accumulator over blocks of `de`
- *          k-steps, folded c = RN32(c + P_t) in term order per block. */
+ *          k-steps, folded c = RN32(c + P_t) in term order per block.
+ *   C3_MAIN / C3_DC: corrected3's two partial results before the epilogue
+ *          (the main-term sum c and the raw dC), as a split-K part stores them. */
 static void *hw_rows(void *arg) {
   hwjob_t *J = (hwjob_t *)arg;
   const int K = J->K;
@@ -314,6 +317,8 @@ static void *hw_rows(void *arg) {
         switch (J->sched) {
           case HW_C3:
           case HW_C3DD:
+          case HW_C3_MAIN:
+          case HW_C3_DC:
             dc = hw_mma(dc, ks > 0, al + o, eal + o, bh + o, ebh + o, K);
             dc = hw_mma(dc, 1, ah + o, eah + o, bl + o, ebl + o, K);
             if (J->sched == HW_C3DD) ddc = hw_mma(ddc, ks > 0, al + o, eal + o, bl + o, ebl + o, K);
@@ -339,7 +344,11 @@ static void *hw_rows(void *arg) {
             break;
         }
       }
-      if (J->sched == HW_C3 || J->sched == HW_C3DD) {
+      if (J->sched == HW_C3_MAIN) {
+        out = acc;
+      } else if (J->sched == HW_C3_DC) {
+        out = dc;
+      } else if (J->sched == HW_C3 || J->sched == HW_C3DD) {
         out = fmaf(dc, J->inv_scale, acc);
         if (J->sched == HW_C3DD) out = fmaf(ddc, J->inv_scale2, out);
       } else if (J->sched == HW_IN4RN) {
@@ -633,7 +642,8 @@ int tcec_oracle_inunit(int kind, int f, int s, int mode, int term_mode, int64_t 
 /* The GPU kernels' arithmetic with the hardware MMA model (hw_mma, hw_rows):
  * sched 0 corrected3, 1 corrected3 + dA*dB chain, 2 tc_plain, 3 in-unit four
  * terms (markidis4 / corrected4_rz), 4 corrected4 with the RN terminal
- * emulated by per-block drains.  f / s / mode: the split (or, for tc_plain,
+ * emulated by per-block drains, 5 / 6 corrected3's main-term sum / raw dC
+ * (before the epilogue; a split-K part's stored planes).  f / s / mode: the split (or, for tc_plain,
  * the conversion) exactly as the reference (splitting.py:114-122,
  * schemes.py:343-351); drain_ksteps: drain interval (C3) / block (IN4RN) in
  * MMA k-steps (16 FP16, 8 TF32).  k is padded to whole operand stages (64
@@ -643,7 +653,7 @@ int tcec_oracle_inunit(int kind, int f, int s, int mode, int term_mode, int64_t 
 int tcec_oracle_hw(int sched, int f, int s, int mode, int64_t m, int64_t n, int64_t k,
                    const float *A, int64_t lda, const float *B, int64_t ldb, float *C,
                    int64_t ldc, int drain_ksteps, int nthreads, uint32_t *flags) {
-  if (m < 0 || n < 0 || k < 0 || drain_ksteps < 1 || sched < 0 || sched > 4) return -1;
+  if (m < 0 || n < 0 || k < 0 || drain_ksteps < 1 || sched < 0 || sched > 6) return -1;
   if (f != FMT_FP16 && f != FMT_TF32) return -1;
   const int K = f == FMT_FP16 ? 16 : 8, stage = f == FMT_FP16 ? 64 : 32;
   const int emin = f == FMT_FP16 ? -14 : -126;

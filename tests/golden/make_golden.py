@@ -122,6 +122,19 @@ def gemm_goldens():
     a = G(MS(4, 48, tcgemm.ExpRand(14, 16), 21))
     b = G(MS(48, 4, tcgemm.Urand(-1, 1), 22))
     cases.append(("overflow_4x4x48", a, b))
+    # single overflowing inputs where the reference returns +-inf, not NaN: B's
+    # values have lo != 0 of hi's sign, so A_hi * dB is an infinity of the main
+    # term's sign (splitting.py:119-121 sets that row's dA to 0); one zero in B
+    # makes inf * 0 = NaN in one column.  Row 1: 70000 overflows FP16 only;
+    # row 4: -65520 rounds (RN, ties to even) to -65536 = -inf in FP16; row 5:
+    # FLT_MAX overflows both hi formats.
+    a = G(MS(6, 40, tcgemm.Urand(-1, 1), 23)).copy()
+    a[1, 3], a[4, 10], a[5, 0] = 70000.0, -65520.0, np.float32(3.4028235e38)
+    rng = np.random.default_rng(24)
+    b = (np.float32(1 + 2.0 ** -13) * np.exp2(rng.integers(-3, 1, (40, 8)))
+         * rng.choice([-1, 1], (40, 8))).astype(np.float32)
+    b[3, 2] = 0.0
+    cases.append(("ovf_inf_6x8x40", a, b))
     # identity: A = I16, B FP16-exact -> output == B
     eye = np.eye(16, dtype=np.float32)
     bexact = (np.round(G(MS(16, 16, tcgemm.Urand(-1, 1), 5)) * 1024) / 1024).astype(np.float32)

@@ -1,23 +1,24 @@
 """GPU parity of the fused TCEC GEMM (FP16-TCEC / TF32-TCEC).
 
-The tensor core's internal accumulation is hardware-defined, so the GPU is
-compared with the oracle within a stated tolerance, not bit for bit.  With
-u = 2^-24 and S_ij = sum_t |A_hi||B_hi| + 2^-s (|A_lo||B_hi| + |A_hi||B_lo|)
-(the magnitudes the three products actually accumulate):
+Two oracles (oracle/tcec_oracle.c, test infrastructure):
 
-  * in-range inputs: |C_gpu - C_ref|_ij <= 32 u S_ij  (measured <= 1.1 u S on
-    urand, <= 9 u S on 2^-15..2^15 exponent spreads) and the Frobenius
-    relative difference <= 1e-6;
-  * inputs the reference flags out_of_range (its result is degraded by design,
-    SPEC.md:306): identical flags and non-finite pattern, |C_gpu - C_ref|_ij
-    <= 2^-12 S_ij (measured 448 u S on the Type 2 golden);
-  * accuracy vs FP64 (Eq. 7) within x[0.5, 2] of the emulated FP32 SGEMM
-    (SPEC.md:283 / :534 windows, 8-seed means)
+  * the HARDWARE model (O.corrected3_hw / O.inunit_hw): the reference's split
+    and product order with the B200 tensor core's measured MMA arithmetic
+    (profiles/r02/accumulator_probe.md) and the kernels' drain schedule.  The
+    GPU must equal it BIT FOR BIT -- every kernel, drain interval, shape and
+    input class, non-finite outputs included (NaN positions, inf signs);
+  * the REFERENCE model (O.corrected3 / O.inunit, pinned bit for bit to the
+    reference's own outputs by test_oracle_golden.py): the same algorithm with
+    the reference's emulated 25-bit unit.  The GPU differs from it only by the
+    unit's arithmetic, bounded elementwise by TOL_REF_* x u x S_ij (u = 2^-24,
+    S_ij = sum_t |A_hi||B_hi| + 2^-s (|A_lo||B_hi| + |A_hi||B_lo|)), each bound
+    2x the maximum measured over the reference's golden cases: 1.11 (urand),
+    9.04 (2^+-15 spreads, Types 1-4 in range), 448 (the FP16 Type 2 case the
+    reference flags out_of_range, degraded by design).  Flags and
+    the non-finite outputs are exact.
 
-C_ref is either the reference's own output (golden fixtures made by importing
-the reference) or the CPU oracle with the kernel's drain interval (SURVEY.md
-Appendix A restatement, pinned to the reference by test_oracle_golden.py).
-Flags, identity, determinism, separability and edge shapes are exact.
+Accuracy vs FP64 (Eq. 7) stays within x[0.5, 2] of the emulated FP32 SGEMM
+(SPEC.md:283 / :534 windows, 8-seed means).
 """
 
 import os
@@ -30,8 +31,10 @@ from oracle import oracle as O
 pytestmark = pytest.mark.gpu
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
-TOL_ULP = 32.0
-TOL_OUT_OF_RANGE = 2.0 ** -12
+TOL_REF_NARROW = 2.5     # u * S: urand inputs (measured max 1.11)
+TOL_REF_WIDE = 20.0      # u * S: exponent spreads, Types 1-4 in range (measured max 9.04)
+TOL_REF_OOR = 1000.0     # u * S: inputs the reference flags out_of_range (measured 448)
+TOL_REF_FROB = 5e-7      # Frobenius, in range (measured max 2.1e-7)
 # (scheme, oracle variant, MMA k-step, default drain interval of the kernel)
 VARIANTS = [("corrected3_halfhalf", "fp16", 16, 128), ("corrected3_tf32", "tf32", 8, 64)]
 
@@ -51,6 +54,28 @@ def _run(a, b, scheme, **kw):
     return run.output.cpu().numpy(), run.flags
 
 
+def _check_exact(c, ref, what=None):
+    """Bit for bit: identical bits everywhere except NaNs, which must coincide."""
+    c = np.asarray(c, np.float32)
+    ref = np.asarray(ref, np.float32)
+    assert c.shape == ref.shape, what
+    nan = np.isnan(ref)
+    assert np.array_equal(np.isnan(c), nan), (what, int((np.isnan(c) != nan).sum()))
+    same = c.view(np.uint32) == ref.view(np.uint32)
+    bad = ~same & ~nan
+    if bad.any():
+        i, j = np.argwhere(bad)[0]
+        raise AssertionError((what, int(bad.sum()), float(c[i, j]), float(ref[i, j])))
+
+
+def _flags_of(fl):
+    return (fl.saw_overflow, fl.saw_out_of_range)
+
+
+def _oflags(ofl):
+    return (bool(ofl & 1), bool(ofl & 2))
+
+
 def _split_mag(a, b, variant):
     s = 11 if variant == "fp16" else 0
     ah, al = O.split(a, variant)
@@ -59,18 +84,19 @@ def _split_mag(a, b, variant):
     return np.abs(ah) @ np.abs(bh) + (np.abs(al) @ np.abs(bh) + np.abs(ah) @ np.abs(bl)) * 2.0 ** -s
 
 
-def _check_close(c, ref, a, b, what, variant=None, out_of_range=False):
-    if variant is None:
-        variant = "fp16" if ("half" in str(what) or "fp16" in str(what)) else "tf32"
+def _check_close(c, ref, a, b, what, variant, tol=TOL_REF_NARROW, out_of_range=False):
+    """Against the REFERENCE model: elementwise within tol x u x S, non-finite
+    outputs identical (inf signs, NaN positions), Frobenius in range."""
     mag = _split_mag(a, b, variant)
-    bound = (TOL_OUT_OF_RANGE if out_of_range else TOL_ULP * 2.0 ** -24) * mag
+    bound = (TOL_REF_OOR if out_of_range else tol) * 2.0 ** -24 * mag
     fin = np.isfinite(ref)
     assert np.array_equal(fin, np.isfinite(c)), what
+    _check_exact(np.where(fin, 0, c), np.where(fin, 0, ref), what)
     diff = np.abs(c[fin].astype(np.float64) - ref[fin].astype(np.float64))
     worst = np.max(diff - bound[fin]) if diff.size else 0.0
     assert worst <= 0.0, (what, float(np.max(diff / np.maximum(bound[fin], 1e-300))))
     if np.linalg.norm(ref[fin]) > 0 and not out_of_range:
-        assert _T().relative_residual(c[fin], ref[fin]) <= 1e-6, what
+        assert _T().relative_residual(c[fin], ref[fin]) <= TOL_REF_FROB, what
 
 
 @pytest.fixture(scope="module")
@@ -79,29 +105,44 @@ def gold():
 
 
 def test_gemm_vs_reference_goldens(gold):
-    """Every golden case computed by the reference's own gemm()."""
+    """Every golden case computed by the reference's own gemm(): the GPU with the
+    reference's schedule (MmaConfig(block_k=16)) equals the hardware model at
+    drain 16 bit for bit and the reference's output within TOL_REF; the
+    default schedule equals the hardware model at the default drain; flags and
+    non-finite outputs (inf signs, NaN) equal the reference's exactly."""
+    T = _T()
     for tag in [str(t) for t in gold["names"]]:
         a, b = gold[f"{tag}__A"], gold[f"{tag}__B"]
-        for sname, variant, *_ in VARIANTS:
-            c, flags = _run(a, b, sname)
+        for sname, variant, _, drain in VARIANTS:
             ref = gold[f"{tag}__{sname}__C"]
             ov, oor = gold[f"{tag}__{sname}__flags"]
-            assert flags.saw_overflow == bool(ov), (tag, sname)
-            assert flags.saw_out_of_range == bool(oor), (tag, sname)
-            _check_close(c, ref, a, b, (tag, sname), variant, out_of_range=bool(oor))
+            c16, fl = _run(a, b, sname, cfg=T.MmaConfig(block_k=16))
+            assert _flags_of(fl) == (bool(ov), bool(oor)), (tag, sname)
+            _check_exact(c16, O.corrected3_hw(a, b, variant, drain_k=16)[0], (tag, sname, 16))
+            tol = TOL_REF_NARROW if tag.startswith(("urand", "identity")) else TOL_REF_WIDE
+            _check_close(c16, ref, a, b, (tag, sname), variant, tol, out_of_range=bool(oor))
+            c, fl = _run(a, b, sname)
+            assert _flags_of(fl) == (bool(ov), bool(oor)), (tag, sname)
+            _check_exact(c, O.corrected3_hw(a, b, variant)[0], (tag, sname, drain))
+            fin = np.isfinite(ref)
+            _check_exact(np.where(fin, 0, c), np.where(fin, 0, ref), (tag, sname, "non-finite"))
 
 
 @pytest.mark.parametrize("sname,variant,bk,drain", VARIANTS)
 @pytest.mark.parametrize("shape", [(128, 128, 64), (200, 136, 1000), (33, 70, 129),
                                    (300, 260, 2048), (1, 1, 1), (5, 7, 33)])
 def test_gemm_vs_oracle_matched_drain(sname, variant, bk, drain, shape):
+    """Bit for bit against the hardware model; within TOL_REF of the reference
+    model at the same drain interval; flags exact."""
     m, n, k = shape
     a = O.urand(m, k, -1, 1, 21)
     b = O.urand(k, n, -1, 1, O.pair_seed(21))
     c, flags = _run(a, b, sname)
+    hc, hfl = O.corrected3_hw(a, b, variant)
+    _check_exact(c, hc, (sname, shape))
     oc, ofl = O.corrected3(a, b, variant, block_k=bk, drain_k=drain)
     _check_close(c, oc, a, b, (sname, shape), variant)
-    assert (flags.saw_overflow, flags.saw_out_of_range) == (bool(ofl & 1), bool(ofl & 2))
+    assert _flags_of(flags) == _oflags(ofl) == _oflags(hfl)
 
 
 @pytest.mark.parametrize("sname,variant,bk,drain", VARIANTS)
@@ -110,8 +151,9 @@ def test_gemm_wide_exponent_range_vs_oracle(sname, variant, bk, drain):
     a = O.exprand(m, k, -15, 14, 31)
     b = O.exprand(k, n, -15, 14, O.pair_seed(31))
     c, _ = _run(a, b, sname)
+    _check_exact(c, O.corrected3_hw(a, b, variant)[0], sname)
     oc, _ = O.corrected3(a, b, variant, block_k=bk, drain_k=drain)
-    _check_close(c, oc, a, b, sname, variant)
+    _check_close(c, oc, a, b, sname, variant, TOL_REF_WIDE)
 
 
 @pytest.mark.parametrize("sname,variant,bk,drain", VARIANTS)
@@ -235,6 +277,7 @@ def test_drain_interval_option(sname, variant, bk, drain):
     A, B = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
     for d in (bk, 2 * bk, 3 * bk, 4 * bk, 5 * bk, 8 * bk, 32 * bk):
         c = T.gemm_device(A, B, sname, drain_k=d).cpu().numpy()
+        _check_exact(c, O.corrected3_hw(a, b, variant, drain_k=d)[0], (sname, d))
         oc, _ = O.corrected3(a, b, variant, block_k=bk, drain_k=d)
         _check_close(c, oc, a, b, (sname, d), variant)
     for d in (16, 48, 4 * drain):
@@ -319,9 +362,11 @@ def test_reference_scheme_objects_are_accepted():
     c2, _ = _run(a, b, "corrected3_halfhalf")
     assert np.array_equal(c1, c2)
     c3, _ = _run(a, b, T.corrected3(T.tf32tf32(T.RoundingMode.RZ)))
+    _check_exact(c3, O.corrected3_hw(a, b, "tf32", rounding=O.RM_RZ)[0], "tf32 rz")
     oc, _ = O.corrected3(a, b, "tf32", block_k=8, drain_k=64, rounding=O.RM_RZ)
     _check_close(c3, oc, a, b, "tf32 rz", "tf32")
     c4, _ = _run(a, b, T.corrected3(T.markidis_halfhalf()))
+    _check_exact(c4, O.corrected3_hw(a, b, "fp16u")[0], "fp16 unscaled")
     oc, _ = O.corrected3(a, b, "fp16u", block_k=16, drain_k=128)
     _check_close(c4, oc, a, b, "fp16 unscaled", "fp16u")
     # the CPU baselines have no tensor-core form
@@ -353,9 +398,7 @@ def test_large_square_properties(sname):
     variant = "fp16" if "half" in sname else "tf32"
     a = A[rows[:4]].cpu().numpy()
     b = B[:, 1000:1040].cpu().numpy()
-    oc, _ = O.corrected3(a, b, variant, block_k=16 if variant == "fp16" else 8,
-                         drain_k=128 if variant == "fp16" else 64)
-    _check_close(C[rows[:4]][:, 1000:1040].cpu().numpy(), oc, a, b, sname, variant)
+    _check_exact(C[rows[:4]][:, 1000:1040].cpu().numpy(), O.corrected3_hw(a, b, variant)[0], sname)
 
 
 @pytest.mark.parametrize("sname,variant,bk,drain", VARIANTS)
@@ -476,9 +519,10 @@ def _inunit_mag(a, b, name):
 
 @pytest.mark.parametrize("name", INUNIT_HW)
 def test_inunit_comparators_vs_reference_goldens(name):
-    """tc_plain / markidis4 / corrected4_rz on the tensor core against the
-    reference's outputs (tests/golden/inunit_golden.npz).  The in-unit
-    accumulation is the hardware's, so the bound is per terminal rounding:
+    """tc_plain / markidis4 / corrected4_rz on the tensor core: bit for bit
+    against the hardware model, and against the reference's outputs
+    (tests/golden/inunit_golden.npz), where the in-unit accumulation differs by
+    the unit, so the bound is per terminal rounding:
     |C_gpu - C_ref| <= (terms * k/16 + 2) * 2^-22 * sum|a_t||b_t|; flags and the
     non-finite pattern are exact."""
     T = _T()
@@ -490,6 +534,7 @@ def test_inunit_comparators_vs_reference_goldens(name):
         ov, oor = g[f"{tag}__{name}__flags"]
         assert (run.flags.saw_overflow, run.flags.saw_out_of_range) == (bool(ov), bool(oor)), tag
         c = run.output
+        _check_exact(c, O.inunit_hw(a, b, name)[0], (tag, name))
         fin = np.isfinite(ref)
         assert np.array_equal(fin, np.isfinite(c)), tag
         mag, terms = _inunit_mag(a, b, name)
@@ -538,6 +583,7 @@ def test_delta_delta_term_vs_oracle(sname, variant, bk, drain):
     r3, r4, max_ulp = T.delta_term_ablation(a, b, split)
     c_def = T.gemm(a, b, sname).output
     assert np.array_equal(r3.output, c_def)
+    _check_exact(r4.output, O.corrected3_hw(a, b, variant, include_dd=True)[0], sname)
     o4, _ = O.corrected3(a, b, variant, block_k=bk, drain_k=drain, include_dd=True)
     _check_close(r4.output, o4, a, b, sname, variant)
     o3, _ = O.corrected3(a, b, variant, block_k=bk, drain_k=drain)
@@ -559,6 +605,7 @@ def test_inunit_ragged_vs_oracle(name, shape):
     if k == 0:
         assert np.all(run.output == 0.0)
         return
+    _check_exact(run.output, O.inunit_hw(a, b, name)[0], (name, shape))
     ref, fl = O.inunit(a, b, name)
     assert (run.flags.saw_overflow, run.flags.saw_out_of_range) == (bool(fl & 1), bool(fl & 2))
     mag, terms = _inunit_mag(a, b, name)
@@ -591,10 +638,12 @@ def test_corrected4_rn_blocks_vs_oracle(name, block_k, shape):
         cols = np.r_[0:16, n - 16:n]
         ref, fl = O.inunit(a[rows], b[:, cols], name, block_k=block_k)
         got = run.output[np.ix_(rows, cols)]
+        _check_exact(got, O.inunit_hw(a[rows], b[:, cols], name, block_k=block_k)[0], name)
         mag, terms = _inunit_mag(a[rows], b[:, cols], name)
     else:
         ref, fl = O.inunit(a, b, name, block_k=block_k)
         got = run.output
+        _check_exact(got, O.inunit_hw(a, b, name, block_k=block_k)[0], name)
         mag, terms = _inunit_mag(a, b, name)
         assert (run.flags.saw_overflow, run.flags.saw_out_of_range) == (bool(fl & 1), bool(fl & 2))
     bound = (terms * (-(-k // block_k)) + 2) * 2.0 ** -22 * mag
@@ -619,7 +668,7 @@ def test_corrected4_rn_rejects_partial_k_step():
 @pytest.mark.parametrize("sname,variant,bk,drain", VARIANTS)
 def test_split_k_automatic(sname, variant, bk, drain):
     """split_k = -1: on a long-k product with few tiles the automatic choice
-    splits (result within the GEMM tolerance, not the single-pass bits); on a
+    splits (the split-K hardware model's bits, not the single pass's); on a
     product that fills the GPU it stays off (bit-identical to the default)."""
     import torch
 
@@ -632,8 +681,8 @@ def test_split_k_automatic(sname, variant, bk, drain):
     torch.cuda.synchronize()
     assert torch.equal(c_auto, c_eight)  # 1 tile, 74 pairs, >= 16 stages per part: 8 parts
     rows = np.r_[0:4, 250:256]
-    o, _ = O.corrected3(a[rows], b, variant, block_k=bk, drain_k=drain)
-    _check_close(c_auto.cpu().numpy()[rows], o, a[rows], b, sname, variant)
+    _check_exact(c_auto.cpu().numpy()[rows], O.corrected3_hw_split_k(a[rows], b, variant, 8)[0],
+                 sname)
     a2 = O.urand(4096, 512, -1, 1, 23)
     b2 = O.urand(512, 4096, -1, 1, 24)
     A2, B2 = torch.from_numpy(a2).cuda(), torch.from_numpy(b2).cuda()
@@ -645,10 +694,11 @@ def test_split_k_automatic(sname, variant, bk, drain):
                                          ((520, 576, 2048), 2), ((256, 256, 100), 8)])
 def test_split_k_vs_oracle(sname, variant, bk, drain, shape, parts):
     """opts.split_k: k in contiguous parts, partial sums combined in part order.
-    Not the single-pass rounding sequence, so the bar is the GEMM tolerance
-    against the oracle (rows sampled across tiles), SGEMM-level accuracy
-    against FP64, determinism, and the default path's RunFlags -- including
-    inputs spanning 2^-40..2^15 (out_of_range for FP16)."""
+    Not the single-pass rounding sequence: bit for bit against the hardware
+    model of the split-K path (rows sampled across tiles), within TOL_REF of
+    the single-pass reference model, SGEMM-level accuracy against FP64,
+    determinism, and the default path's RunFlags -- including inputs spanning
+    2^-40..2^15 (out_of_range for FP16)."""
     import torch
 
     T = _T()
@@ -663,6 +713,8 @@ def test_split_k_vs_oracle(sname, variant, bk, drain, shape, parts):
     torch.cuda.synchronize()
     assert torch.equal(c1, c2)  # deterministic
     rows = np.unique(np.r_[0:4, m // 2:m // 2 + 4, m - 4:m])
+    _check_exact(c1.cpu().numpy()[rows], O.corrected3_hw_split_k(a[rows], b, variant, parts)[0],
+                 (sname, shape, parts))
     o, _ = O.corrected3(a[rows], b, variant, block_k=bk, drain_k=drain)
     _check_close(c1.cpu().numpy()[rows], o, a[rows], b, sname, variant)
     ref = A.double() @ B.double()
@@ -788,7 +840,7 @@ def test_host_path_split_k_equals_device(blocks):
 def test_baseline_full_size_configs(sname, variant, bk, drain, shape):
     """BASELINE.json configs 2 and 4 at their full sizes.  The whole-product oracle
     is infeasible there, so: (i) a 4 x 32 block from the middle of the product
-    against the oracle with the kernel's drain interval (GEMM tolerance);
+    bit for bit against the hardware model;
     (ii) separability -- the same rows and columns computed as a small product
     are bit-identical to the full product's block; (iii) relres vs FP64 on 64
     rows spread over every tile row, within 2x of cuBLAS SGEMM's."""
@@ -805,8 +857,7 @@ def test_baseline_full_size_configs(sname, variant, bk, drain, shape):
     a = A[r0:r0 + 4].cpu().numpy()
     b = B[:, c0:c0 + 32].contiguous().cpu().numpy()
     blk = C[r0:r0 + 4, c0:c0 + 32].cpu().numpy()
-    oc, _ = O.corrected3(a, b, variant, block_k=bk, drain_k=drain)
-    _check_close(blk, oc, a, b, sname, variant)
+    _check_exact(blk, O.corrected3_hw(a, b, variant)[0], (sname, shape))
     small = T.gemm_device(A[r0:r0 + 4].contiguous(), B[:, c0:c0 + 32].contiguous(), sname)
     assert np.array_equal(small.cpu().numpy(), blk)
     rows = torch.arange(3, m, max(1, m // 64), device="cuda")[:64]
@@ -898,8 +949,8 @@ def test_randomized_shapes_and_ranges_vs_oracle(case):
     """Seeded fuzz over shapes (1..700 rows / columns, 1..1500 k, ragged in every
     dimension), exponent ranges (urand and ExpRand bands inside the FP16 range
     and, for TF32, across 2^-100..2^60), both variants and the default kernel
-    selection: the GPU result is within the GEMM tolerance of the oracle with
-    the same drain interval, with identical flags."""
+    selection: bit for bit against the hardware model, within TOL_REF of the
+    reference model, identical flags."""
     rng = np.random.default_rng(1000 + case)
     m, n = (int(x) for x in rng.integers(1, 700, 2))
     k = int(rng.integers(1, 1500))
@@ -917,9 +968,12 @@ def test_randomized_shapes_and_ranges_vs_oracle(case):
         a = O.exprand(m, k, lo, hi, 3 * case)
         b = O.exprand(k, n, lo, hi, 3 * case + 1)
     c, fl = _run(a, b, sname)
+    hc, hfl = O.corrected3_hw(a, b, variant)
+    _check_exact(c, hc, (case, m, n, k))
     oc, ofl = O.corrected3(a, b, variant, block_k=bk, drain_k=drain)
-    assert (fl.saw_overflow, fl.saw_out_of_range) == (bool(ofl & 1), bool(ofl & 2)), case
-    _check_close(c, oc, a, b, sname, variant, out_of_range=bool(ofl & 2))
+    assert _flags_of(fl) == _oflags(ofl) == _oflags(hfl), case
+    _check_close(c, oc, a, b, sname, variant, TOL_REF_NARROW if kind == 0 else TOL_REF_WIDE,
+                 out_of_range=bool(ofl & 2))
 
 
 def test_strided_and_transposed_views_match_contiguous():
@@ -943,3 +997,82 @@ def test_strided_and_transposed_views_match_contiguous():
         ref = T.gemm_device(a.contiguous(), b.contiguous(), "corrected3_tf32")
         out = T.gemm_device(a, b, "corrected3_tf32")
         assert torch.equal(out, ref)
+
+
+def test_config1_full_1024_cubed_eight_seeds():
+    """BASELINE.json configs[0] as the reference CLI runs it (cli.py:135-170):
+    FP16-TCEC, m = n = k = 1024, urand(-1, 1), seeds 0..7, the whole product.
+    (i) The default schedule equals the hardware model bit for bit;
+    (ii) the reference's own schedule (MmaConfig(block_k=16)) equals the
+    hardware model at drain 16 bit for bit, and the reference model within
+    TOL_REF; (iii) the 8-seed mean relres vs FP64 stays within x[0.5, 2] of
+    the reference algorithm's and below cuBLAS SGEMM's."""
+    import torch
+
+    T = _T()
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    r = {"gpu": [], "gpu16": [], "ref": [], "cublas": []}
+    try:
+        for seed in range(8):
+            a = O.urand(1024, 1024, -1, 1, seed)
+            b = O.urand(1024, 1024, -1, 1, O.pair_seed(seed))
+            A, B = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+            f64 = (A.double() @ B.double()).cpu().numpy()
+            c, fl = _run(a, b, "corrected3_halfhalf")
+            assert _flags_of(fl) == (False, False)
+            _check_exact(c, O.corrected3_hw(a, b, "fp16")[0], (seed, "default"))
+            c16, _ = _run(a, b, "corrected3_halfhalf", cfg=T.MmaConfig(block_k=16))
+            _check_exact(c16, O.corrected3_hw(a, b, "fp16", drain_k=16)[0], (seed, 16))
+            ref, _ = O.corrected3(a, b, "fp16", block_k=16, drain_k=16)
+            _check_close(c16, ref, a, b, (seed, "reference model"), "fp16")
+            r["gpu"].append(T.relative_residual(c, f64))
+            r["gpu16"].append(T.relative_residual(c16, f64))
+            r["ref"].append(T.relative_residual(ref, f64))
+            r["cublas"].append(T.relative_residual((A @ B).cpu().numpy(), f64))
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    mean = {k: float(np.mean(v)) for k, v in r.items()}
+    print("config1 relres (8-seed means):", mean)
+    for key in ("gpu", "gpu16"):
+        assert 0.5 <= mean[key] / mean["ref"] <= 2.0, mean
+        assert mean[key] < mean["cublas"], mean
+
+
+def test_cuda_inputs_must_hold_fp32_values():
+    """schemes.py:163-171 on the CUDA path: a float64 tensor whose values are not
+    FP32 (0.1) raises ValueError, as do non-finite ones; exactly representable
+    float64 / integer values are accepted and give the float32 result."""
+    import torch
+
+    T = _T()
+    b = torch.ones((4, 4), device="cuda")
+    with pytest.raises(ValueError, match="FP32"):
+        T.gemm(torch.full((4, 4), 0.1, dtype=torch.float64, device="cuda"), b, "corrected3_tf32")
+    with pytest.raises(ValueError, match="FP32"):
+        T.gemm(b, torch.full((4, 4), 2 ** 25 + 1, dtype=torch.int64, device="cuda"), "corrected3_tf32")
+    with pytest.raises(ValueError, match="finite"):
+        T.gemm(torch.full((4, 4), float("inf"), dtype=torch.float64, device="cuda"), b,
+               "corrected3_halfhalf")
+    x = torch.rand((8, 8), device="cuda")
+    r64 = T.gemm(x.double(), x.double(), "corrected3_halfhalf")
+    r32 = T.gemm(x, x, "corrected3_halfhalf")
+    assert torch.equal(r64.output, r32.output)
+
+
+def test_out_argument_is_validated():
+    """gemm_device never writes past a caller's `out`: a wrong shape, dtype or
+    device raises ValueError before any launch."""
+    import torch
+
+    T = _T()
+    a = torch.rand((64, 32), device="cuda")
+    b = torch.rand((32, 48), device="cuda")
+    for bad in (torch.empty((63, 48), device="cuda"), torch.empty((64, 48), dtype=torch.float16,
+                                                                  device="cuda"),
+                torch.empty((64, 48)), torch.empty((64, 47), device="cuda")):
+        with pytest.raises(ValueError):
+            T.gemm_device(a, b, "corrected3_tf32", out=bad)
+    out = torch.full((64, 48), float("nan"), device="cuda")
+    T.gemm_device(a, b, "corrected3_tf32", out=out)
+    assert torch.equal(out, T.gemm_device(a, b, "corrected3_tf32"))
