@@ -1,12 +1,16 @@
 """Benchmark of the B200 error-corrected SGEMM (FP16-TCEC / TF32-TCEC).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--variant tf32|fp16] [--n 16384] [--allgather]
+                    [--variant tf32|fp16] [--n 16384] [--dist exprand:-50,50|urand]
+                    [--allgather]
 
 One step = one error-corrected GEMM of the workload (default: TF32-TCEC,
-m = n = k = 16384, BASELINE.json configs[1] at the size its metric is quoted
-on).  Inputs are 1 GiB FP32 matrices each (> the 126 MB L2), so no L2 flush is
-needed between steps.  Under torchrun (N > 1) every rank computes its own
+m = n = k = 16384 on BASELINE.json configs[1]'s "full FP32 exponent range"
+inputs: ExpRand(-50, 50) -- the reference's generator genmat.py:39-52 / :83-89,
+sign x 2^e x [1, 2) with e uniform on [-50, 50], the widest band for which
+a_max + b_max + log2 k < 127 keeps every sum finite).  urand(-1, 1) results
+are reported beside it (extras).  Inputs are 1 GiB FP32 matrices each (> the
+126 MB L2), so no L2 flush is needed between steps.  Under torchrun (N > 1) every rank computes its own
 16384-row slab of an (N*16384) x 16384 x 16384 product with B replicated
 (weak scaling, no data-path collective; --allgather adds the optional NCCL
 all-gather of C inside the timed region).
@@ -54,6 +58,8 @@ def parse():
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--variant", choices=["tf32", "fp16"], default="tf32")
     p.add_argument("--n", type=int, default=16384)
+    p.add_argument("--dist", default=None,
+                   help="urand | exprand:a,b (default: exprand:-50,50 for tf32, urand for fp16)")
     p.add_argument("--m-total", type=int, default=0,
                    help="strong scaling: total rows of A / C split over the ranks "
                         "(BASELINE configs[4]: --m-total 65536 --n 65536); default: n rows per rank")
@@ -67,7 +73,50 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-extras", action="store_true", help="skip cuBLAS / accuracy / other variant")
     p.add_argument("--cpu-sample-seconds", type=float, default=15.0)
-    return p.parse_args()
+    args = p.parse_args()
+    if args.dist is None:
+        args.dist = "exprand:-50,50" if args.variant == "tf32" else "urand"
+    args.dist_spec = parse_dist(args.dist)
+    return args
+
+
+def parse_dist(text: str):
+    """('urand',) or ('exprand', a, b)."""
+    if text in ("urand", "urand:-1,1"):
+        return ("urand",)
+    if text.startswith("exprand:"):
+        a, b = (int(x) for x in text.split(":", 1)[1].split(","))
+        if not -126 <= a <= b <= 127:
+            raise SystemExit("exprand exponents must lie in [-126, 127]")
+        return ("exprand", a, b)
+    raise SystemExit(f"unknown --dist {text!r}")
+
+
+def dist_label(spec) -> str:
+    return "urand(-1,1)" if spec[0] == "urand" else f"ExpRand({spec[1]},{spec[2]})"
+
+
+def device_matrix(spec, rows: int, cols: int, gen, dev):
+    """Synthetic FP32 inputs on the device (torch Philox): urand(-1, 1), or
+    ExpRand(a, b) as its FP32 bit pattern -- sign, biased exponent a..b,
+    uniform 23-bit mantissa (the reference's ExpRand, genmat.py:83-89)."""
+    import torch
+
+    if spec[0] == "urand":
+        return (torch.rand((rows, cols), generator=gen, device=dev) * 2 - 1).contiguous()
+    _, a, b = spec
+    e = torch.randint(a + 127, b + 128, (rows, cols), generator=gen, device=dev, dtype=torch.int32)
+    mant = torch.randint(0, 1 << 23, (rows, cols), generator=gen, device=dev, dtype=torch.int32)
+    sign = torch.randint(0, 2, (rows, cols), generator=gen, device=dev, dtype=torch.int32)
+    return ((sign << 31) | (e << 23) | mant).view(torch.float32).contiguous()
+
+
+def host_matrix(spec, rows: int, cols: int, seed: int):
+    from oracle import oracle as O
+
+    if spec[0] == "urand":
+        return O.urand(rows, cols, -1, 1, seed)
+    return O.exprand(rows, cols, spec[1], spec[2], seed)
 
 
 def load_peaks():
@@ -202,21 +251,22 @@ class NvmlClockSampler:
 
 
 # ------------------------------------------------------------ CPU oracle ---
-def cpu_oracle_sample(variant: str, k: int, seconds: float, threads: int, rows: int | None = None):
+def cpu_oracle_sample(variant: str, k: int, seconds: float, threads: int, rows: int | None = None,
+                      spec=("urand",)):
     """Time the CPU oracle (test-infrastructure restatement of the reference's
     corrected3 path, oracle/tcec_oracle.c) on a sub-block rows x cols x k of
     the workload, sized to take about `seconds` on `threads` host threads."""
     from oracle import oracle as O
 
-    bk = 16 if variant == "fp16" else 8
+    bk = 16
     cols = 64
     # grow the output block until one run takes about `seconds` (per-call fixed
     # costs -- splitting B, thread start-up -- dominate tiny calibration runs)
     fixed = rows is not None
     rows = rows or threads
     while True:
-        a = O.urand(rows, k, -1, 1, 12)
-        b = O.urand(k, cols, -1, 1, O.pair_seed(12))
+        a = host_matrix(spec, rows, k, 12)
+        b = host_matrix(spec, k, cols, O.pair_seed(12))
         t0 = time.perf_counter()
         O.corrected3(a, b, variant, block_k=bk, nthreads=threads)
         dt = time.perf_counter() - t0
@@ -226,8 +276,9 @@ def cpu_oracle_sample(variant: str, k: int, seconds: float, threads: int, rows: 
         rows = min(16384, int(rows * grow) // threads * threads or threads)
     flops = 2.0 * rows * cols * k
     return {"value": flops / dt / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "port",
-            "sample": f"oracle corrected3 ({variant}) on a {rows}x{cols} output block at k={k} "
-                      f"({dt:.1f} s); full reference algorithm per output",
+            "sample": f"oracle corrected3 ({variant}, the reference's schedule block_k=16) on a "
+                      f"{rows}x{cols} output block at k={k}, {dist_label(spec)} ({dt:.1f} s); "
+                      "full reference algorithm per output",
             "seconds": dt, "rows": rows}
 
 
@@ -243,7 +294,7 @@ def run_reference(args):
     steps_s = min(args.cpu_sample_seconds, max(1.0, 60.0 / max(1, args.steps + args.warmup)))
     rows = None
     for i in range(args.warmup + args.steps):
-        r = cpu_oracle_sample(args.variant, args.n, steps_s, threads, rows)
+        r = cpu_oracle_sample(args.variant, args.n, steps_s, threads, rows, args.dist_spec)
         rows = r["rows"]
         if i >= args.warmup:
             vals.append(r["value"])
@@ -253,10 +304,11 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": sample["seconds"] * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic urand(-1,1)",
+        "vs_baseline": None, "dtype": "f32", "data": f"synthetic {dist_label(args.dist_spec)}",
         "config": {"workload": f"{'TF32' if args.variant == 'tf32' else 'FP16'}-TCEC SGEMM "
                                f"m=n=k={args.n} (bounded output sub-block on host cores)",
-                   "variant": args.variant, "m": args.n, "n": args.n, "k": args.n},
+                   "variant": args.variant, "m": args.n, "n": args.n, "k": args.n,
+                   "dist": dist_label(args.dist_spec)},
         "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": threads, "kind": "port",
                          "sample": sample["sample"]},
         "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -292,10 +344,11 @@ def main():
     mr = -(-args.m_total // world) if args.m_total > 0 else n  # rows of A / C on this rank
     scheme = SCHEME[args.variant]
     gen = torch.Generator(device=dev)
+    spec = args.dist_spec
     gen.manual_seed(1234 + rank)
-    A = (torch.rand((mr, n), generator=gen, device=dev) * 2 - 1).contiguous()
+    A = device_matrix(spec, mr, n, gen, dev)
     gen.manual_seed(99)  # B replicated: identical on every rank
-    B = (torch.rand((n, n), generator=gen, device=dev) * 2 - 1).contiguous()
+    B = device_matrix(spec, n, n, gen, dev)
     C = torch.empty((mr, n), device=dev)
     Cfull = torch.empty((mr * world, n), device=dev) if (args.allgather and world > 1) else None
     stream = torch.cuda.current_stream(dev)
@@ -375,12 +428,13 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
         "higher_is_better": True, "scaling": "strong" if args.m_total > 0 else "weak",
         "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic urand(-1,1) FP32 (torch Philox on device)",
+        "data": f"synthetic {dist_label(spec)} FP32 (torch Philox on device)",
         "config": {"workload": (f"{'TF32' if args.variant == 'tf32' else 'FP16'}-TCEC SGEMM "
                                 + (f"m={mr * world} n=k={n}, {mr} rows per rank" if args.m_total > 0
                                    else f"m=n=k={n} per rank")
                                 + (", row-sharded" if world > 1 else "")),
                    "variant": args.variant, "scheme": scheme, "m": mr * world, "n": n, "k": n,
+                   "dist": dist_label(spec),
                    "parallelism": f"row-shard x{world}" + (
                        (" + fused all-gather C (epilogue peer stores)" if args.fused_allgather
                         else " + all-gather C") if Cfull is not None else ""),
@@ -409,15 +463,18 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize()
         extras["cublas_sgemm_tflops"] = flops_step / (e0.elapsed_time(e1) / reps * 1e-3) / 1e12
-        # accuracy vs FP64 on a 256-row sub-block (relative residual, Eq. 7)
+        # accuracy vs FP64 on a 256-row sub-block (relative residual, Eq. 7) on the
+        # workload's inputs; FP16-TCEC only where its split range holds them
         rows = slice(0, 256)
         ref = torch.matmul(A[rows].double(), B.double())
         acc = {}
-        for v in ("tf32", "fp16"):
-            Cv = T.gemm_device(A, B, SCHEME[v])
-            acc[f"relres_{v}_tcec"] = float(torch.linalg.norm(ref - Cv[rows].double()) / torch.linalg.norm(ref))
+        fp16_ok = spec[0] == "urand" or (spec[1] >= -15 and spec[2] <= 14)
+        for v in ("tf32", "fp16") if fp16_ok else ("tf32",):
+            Cv = T.gemm_device(A[rows].contiguous(), B, SCHEME[v])
+            acc[f"relres_{v}_tcec"] = float(torch.linalg.norm(ref - Cv.double()) / torch.linalg.norm(ref))
         Cs = torch.matmul(A[rows], B)
         acc["relres_cublas_sgemm"] = float(torch.linalg.norm(ref - Cs.double()) / torch.linalg.norm(ref))
+        acc["inputs"] = dist_label(spec)
         extras["accuracy_vs_fp64_256rows"] = acc
         # in-run tensor-core peaks from cuBLAS (denominator context): fp16 and tf32
         # dense 8192^3, best of 5
@@ -439,29 +496,33 @@ def main():
             return 2 * 8192 ** 3 / (best * 1e-3) / 1e12
         extras["cublas_fp16_dense_tflops"] = _peak(torch.float16, False)
         extras["cublas_tf32_dense_tflops"] = _peak(torch.float32, True)
-        # the other variant's throughput (same procedure)
-        other = "fp16" if args.variant == "tf32" else "tf32"
-        for _ in range(2):
-            T.gemm_device(A, B, SCHEME[other], out=C)
-        torch.cuda.synchronize()
-        e0.record(stream)
-        for _ in range(max(3, args.steps // 2)):
-            T.gemm_device(A, B, SCHEME[other], out=C)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        ms_o = e0.elapsed_time(e1) / max(3, args.steps // 2)
-        extras[f"{other}_tcec_tflops"] = flops_step / (ms_o * 1e-3) / 1e12
-        # split-once mode (separate split pass + three-product GEMM; opt-in)
-        for v in ("tf32", "fp16"):
+        # the other input distribution and variant (same procedure); FP16-TCEC on
+        # urand (ExpRand(-50, 50) lies outside its split's range by design)
+        def _time(a, b, sname, reps, **kw):
             for _ in range(2):
-                T.gemm_device(A, B, SCHEME[v], out=C, split_mode=2)
+                T.gemm_device(a, b, sname, out=C, **kw)
             torch.cuda.synchronize()
             e0.record(stream)
-            for _ in range(3):
-                T.gemm_device(A, B, SCHEME[v], out=C, split_mode=2)
+            for _ in range(reps):
+                T.gemm_device(a, b, sname, out=C, **kw)
             e1.record(stream)
             torch.cuda.synchronize()
-            extras[f"{v}_tcec_split_once_tflops"] = flops_step / (e0.elapsed_time(e1) / 3 * 1e-3) / 1e12
+            return flops_step / (e0.elapsed_time(e1) / reps * 1e-3) / 1e12
+
+        reps = max(3, args.steps // 2)
+        if spec[0] != "urand":
+            gen.manual_seed(4321)
+            Au = device_matrix(("urand",), mr, n, gen, dev)
+            Bu = device_matrix(("urand",), n, n, gen, dev)
+        else:
+            Au, Bu = A, B
+        extras[f"{args.variant}_tcec_urand_tflops"] = _time(Au, Bu, scheme, reps)
+        other = "fp16" if args.variant == "tf32" else "tf32"
+        extras[f"{other}_tcec_urand_tflops"] = _time(Au, Bu, SCHEME[other], reps)
+        # split-once mode (separate split pass + three-product GEMM; opt-in)
+        for v in ("tf32", "fp16"):
+            extras[f"{v}_tcec_split_once_urand_tflops"] = _time(Au, Bu, SCHEME[v], 3, split_mode=2)
+        del Au, Bu
         line["extras"] = extras
         del Cs, ref
 
@@ -498,7 +559,7 @@ def main():
 
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_oracle_sample(args.variant, n, args.cpu_sample_seconds,
-                                                 os.cpu_count() or 1)
+                                                 os.cpu_count() or 1, spec=spec)
         line["cpu_baseline"].pop("seconds", None)
         line["cpu_baseline"].pop("rows", None)
 

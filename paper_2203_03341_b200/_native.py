@@ -94,7 +94,8 @@ def lib() -> ctypes.CDLL:
     L.tcec_split.restype = i32
     L.tcec_split.argtypes = [i32, i32, i32, p, i64, p, p, p, p]
     L.tcec_launch_count.restype = u64
-    L.tcec_host_release.restype = i32
+    if hasattr(L, "tcec_host_release"):  # (absent from round-1 builds used in A/B runs)
+        L.tcec_host_release.restype = i32
     _lib = L
     return L
 

@@ -68,40 +68,55 @@ struct PairCfg {
 // the main-term block of schemes.py:300-304 with block_k = de x MMA-K: the
 // first main product of an interval waits until the drain warps have read the
 // previous interval (p_empty) and starts from zero, the last one commits
-// p_full.  j0 is the stage's first k-step within the unit of work, nks the
-// unit's k-steps, git the interval counter (running across tiles).  With
-// stage-aligned intervals the stage's corrections go first, so the drain of
-// the previous P overlaps them; otherwise each k-step's corrections precede its
-// main product.  The order of products into each accumulator is the same
+// p_full.  `pos` counts the k-steps issued into the current interval (0 at a
+// unit's start; the unit's last k-step, j0 + ks == nks - 1, closes its last
+// interval and resets it), git the intervals committed (running across
+// tiles); op_empty is committed once the stage's products are issued.  No
+// division on the issue path: the single MMA thread feeds the tensor pipe.
+// With stage-aligned intervals the stage's corrections go first, so the drain
+// of the previous P overlaps them; otherwise each k-step's corrections precede
+// its main product.  The order of products into each accumulator is the same
 // either way.
 template <typename Corr, typename Main>
-__device__ __forceinline__ void c3_stage(int j0, int nks, int de, uint32_t& git, uint64_t* p_empty,
-                                         uint64_t* p_full, Corr corr, Main mainp) {
-  auto main_step = [&](int ks) {
-    const int j = j0 + ks;
-    const bool first = j % de == 0;
+__device__ __forceinline__ void c3_stage(int j0, int nks, int de, int& pos, uint32_t& git,
+                                         uint64_t* p_empty, uint64_t* p_full, uint64_t* op_empty,
+                                         Corr corr, Main mainp) {
+  if ((de & 3) == 0) {
+    // whole stages per interval: straight-line issue (the tensor pipe is fed by
+    // this one thread; a branch between the main products costs throughput)
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) corr(ks);
+    const bool first = pos == 0;
     if (first && git > 0) {
       sm100::mbar_wait_cluster(p_empty, (git - 1) & 1);
       sm100::tc_fence_after();
     }
-    mainp(ks, first ? 0u : 1u);
-    if (j % de == de - 1 || j == nks - 1) {
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) mainp(ks, (first && ks == 0) ? 0u : 1u);
+    sm100::mma_commit_pair_mc(op_empty, 0x3);
+    pos += 4;
+    if (pos == de || j0 + 4 >= nks) {
       sm100::mma_commit_pair_mc(p_full, 0x3);
       ++git;
+      pos = 0;
     }
-  };
-  if (de % 4 == 0) {
+    return;
+  }
 #pragma unroll
-    for (int ks = 0; ks < 4; ++ks) corr(ks);
-#pragma unroll
-    for (int ks = 0; ks < 4; ++ks) main_step(ks);
-  } else {
-#pragma unroll
-    for (int ks = 0; ks < 4; ++ks) {
-      corr(ks);
-      main_step(ks);
+  for (int ks = 0; ks < 4; ++ks) {
+    corr(ks);
+    if (pos == 0 && git > 0) {
+      sm100::mbar_wait_cluster(p_empty, (git - 1) & 1);
+      sm100::tc_fence_after();
+    }
+    mainp(ks, pos == 0 ? 0u : 1u);
+    if (++pos == de || j0 + ks == nks - 1) {
+      sm100::mma_commit_pair_mc(p_full, 0x3);
+      ++git;
+      pos = 0;
     }
   }
+  sm100::mma_commit_pair_mc(op_empty, 0x3);
 }
 
 // Split one 32-deep FP32 slice of this CTA's A rows and B columns into the
@@ -111,80 +126,61 @@ __device__ __forceinline__ void c3_stage(int j0, int nks, int de, uint32_t& git,
 //   B: k = t & 31, n in [16 (t >> 5), +16)             -> MN-major hi / lo
 // With kFlags the thread also folds its inputs into the RunFlags accumulator
 // (only the CTAs designated to cover each element of A / B exactly once).
-// 16 consecutive values -> hi / lo operand words (FP16: 8 packed half2 each;
-// TF32: 16 floats each, stored as their bit patterns).
+// One 16-byte operand chunk of hi and of lo words from consecutive inputs
+// (FP16: 8 values -> 4 packed half2 words each; TF32: 4 values -> 4 words,
+// the rounded FP32 bit patterns), splitting.py:114-122:
+//   hi = round(x), lo = round((x - hi) 2^s), lo = 0 where hi overflowed
+// (a select per element: measured cheaper than guarding a rare fix-up with a
+// max over the inputs, which costs the 56-register split warps more).
 template <int V, int R>
-__device__ __forceinline__ void split16(const float (&x)[16], float scale, uint32_t (&hw)[16],
-                                        uint32_t (&lw)[16]) {
+__device__ __forceinline__ void split_chunk(const float* x, float scale, uint32_t (&hw)[4],
+                                            uint32_t (&lw)[4]) {
+  constexpr bool kFix = R != kRZ;  // RZ saturates: hi never overflows
   if constexpr (V == kFP16) {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < 4; ++j) {
       hw[j] = cvt_f16x2<R>(x[2 * j], x[2 * j + 1]);
       float h0, h1, r0, r1;
       unpack_f16x2(hw[j], h0, h1);
       sm100::residual_x2(x[2 * j], x[2 * j + 1], h0, h1, scale, r0, r1);
-      // splitting.py:119-121: lo = 0 where hi overflowed (the residual
-      // formula would give -+inf or NaN there)
-      r0 = isinf(h0) ? 0.0f : r0;
-      r1 = isinf(h1) ? 0.0f : r1;
+      if constexpr (kFix) {
+        r0 = isinf(h0) ? 0.0f : r0;
+        r1 = isinf(h1) ? 0.0f : r1;
+      }
       lw[j] = cvt_f16x2<R>(r0, r1);
     }
   } else {
 #pragma unroll
-    for (int j = 0; j < 16; j += 2) {
+    for (int j = 0; j < 4; j += 2) {
       hw[j] = tf32_round_bits<R>(__float_as_uint(x[j]));
       hw[j + 1] = tf32_round_bits<R>(__float_as_uint(x[j + 1]));
-      // splitting.py:119-121: where hi overflowed the residual is x - x = 0
-      const float h0 = __uint_as_float(hw[j]), h1 = __uint_as_float(hw[j + 1]);
+      float h0 = __uint_as_float(hw[j]), h1 = __uint_as_float(hw[j + 1]);
+      if constexpr (kFix) {
+        h0 = isinf(h0) ? x[j] : h0;
+        h1 = isinf(h1) ? x[j + 1] : h1;
+      }
       float r0, r1;
-      sm100::sub_x2(x[j], x[j + 1], isinf(h0) ? x[j] : h0, isinf(h1) ? x[j + 1] : h1, r0, r1);
+      sm100::sub_x2(x[j], x[j + 1], h0, h1, r0, r1);
       lw[j] = tf32_round_bits<R>(__float_as_uint(r0));
       lw[j + 1] = tf32_round_bits<R>(__float_as_uint(r1));
     }
   }
 }
 
-// Split this thread's share of one 32-deep FP32 slice into the operand stage.
-//   kB = false: A row t & 127, k in [16 (t >> 7), +16) -> K-major SW128 hi / lo
-//   kB = true:  B k-row t & 31, n in [16 (t >> 5), +16) -> MN-major hi / lo
-//               (SW128 for FP16, SW128_BASE32B for TF32)
-// With kFlags the inputs are folded into the RunFlags accumulator (only the
-// CTAs designated to classify each element of A / B exactly once).
-template <int V, int R, bool kFlags, bool kB>
-__device__ __forceinline__ void pair_split_regs(const float (&x)[16], uint32_t op, int sub, int t,
-                                                float scale, FlagAcc& fa) {
-  using C = PairCfg<V>;
-  if constexpr (kFlags) {
+// 16 consecutive values -> hi / lo operand words (FP16: 8 packed half2 each;
+// TF32: 16 floats each, stored as their bit patterns).
+template <int V, int R>
+__device__ __forceinline__ void split16(const float (&x)[16], float scale, uint32_t (&hw)[16],
+                                        uint32_t (&lw)[16]) {
+  constexpr int EPC = V == kFP16 ? 8 : 4;  // inputs per chunk
 #pragma unroll
-    for (int i = 0; i < 16; ++i) fa.add(x[i]);
-  }
-  const uint32_t hi_base = op + (kB ? 2 * C::OP_A_BYTES : 0);
-  const uint32_t lo_base = hi_base + (kB ? C::OP_B_BYTES : C::OP_A_BYTES);
-  uint32_t hw[16], lw[16];
-  split16<V, R>(x, scale, hw, lw);
-  constexpr int NCH = V == kFP16 ? 2 : 4;
-  if constexpr (!kB) {
-    const int row = t & 127, half = t >> 7;
-    const int chunk_first = V == kFP16 ? sub * 4 + half * 2 : half * 4;
+  for (int q = 0; q < 16 / EPC; ++q) {
+    uint32_t h[4], l[4];
+    split_chunk<V, R>(x + q * EPC, scale, h, l);
 #pragma unroll
-    for (int q = 0; q < NCH; ++q) {
-      const uint32_t off = sw128(row, chunk_first + q);
-      sm100::sts128(hi_base + off, hw[4 * q], hw[4 * q + 1], hw[4 * q + 2], hw[4 * q + 3]);
-      sm100::sts128(lo_base + off, lw[4 * q], lw[4 * q + 1], lw[4 * q + 2], lw[4 * q + 3]);
-    }
-  } else {
-    const int row = t & 31, qn = t >> 5;
-    const int chunk_first = ((qn * 16) % C::B_ATOM_N) * (V == kFP16 ? 2 : 4) / 16;
-    const int kop = sub * 32 + row;
-    const int grp = kop / C::B_ROWS, rr = kop % C::B_ROWS;
-    const uint32_t base = grp * C::B_SBO + ((qn * 16) / C::B_ATOM_N) * C::B_LBO + rr * 128;
-#pragma unroll
-    for (int q = 0; q < NCH; ++q) {
-      const int c16 = chunk_first + q;
-      const uint32_t off = V == kFP16 ? base + ((c16 ^ rr) << 4)
-                                      : base + ((((c16 >> 1) ^ rr) & 3) << 5) + ((c16 & 1) << 4);
-      sm100::sts128(hi_base + off, hw[4 * q], hw[4 * q + 1], hw[4 * q + 2], hw[4 * q + 3]);
-      sm100::sts128(lo_base + off, lw[4 * q], lw[4 * q + 1], lw[4 * q + 2], lw[4 * q + 3]);
+    for (int j = 0; j < 4; ++j) {
+      hw[4 * q + j] = h[j];
+      lw[4 * q + j] = l[j];
     }
   }
 }
@@ -226,15 +222,17 @@ __device__ __forceinline__ void pair_split_part(uint32_t stg, uint32_t op, int s
   }
   const uint32_t hi_base = op + (kB ? 2 * C::OP_A_BYTES : 0);
   const uint32_t lo_base = hi_base + (kB ? C::OP_B_BYTES : C::OP_A_BYTES);
-  uint32_t hw[16], lw[16];
-  split16<V, R>(x, scale, hw, lw);
   constexpr int NCH = V == kFP16 ? 2 : 4;  // 16-byte chunks per 16 values
+  constexpr int EPC = 16 / NCH;            // inputs per chunk
+  // split and store chunk by chunk: few live registers in the 56-register split warps
   if constexpr (!kB) {
 #pragma unroll
     for (int q = 0; q < NCH; ++q) {
+      uint32_t hw[4], lw[4];
+      split_chunk<V, R>(x + q * EPC, scale, hw, lw);
       const uint32_t off = sw128(row, chunk_first + q);
-      sm100::sts128(hi_base + off, hw[4 * q], hw[4 * q + 1], hw[4 * q + 2], hw[4 * q + 3]);
-      sm100::sts128(lo_base + off, lw[4 * q], lw[4 * q + 1], lw[4 * q + 2], lw[4 * q + 3]);
+      sm100::sts128(hi_base + off, hw[0], hw[1], hw[2], hw[3]);
+      sm100::sts128(lo_base + off, lw[0], lw[1], lw[2], lw[3]);
     }
   } else {
     const int kop = sub * 32 + row;  // k within the operand stage
@@ -243,12 +241,14 @@ __device__ __forceinline__ void pair_split_part(uint32_t stg, uint32_t op, int s
     const int h = V == kTF32 ? (t >> 2) & 1 : 0;  // chunk order, see the loads above
 #pragma unroll
     for (int q = 0; q < NCH; ++q) {
+      uint32_t hw[4], lw[4];
+      split_chunk<V, R>(x + q * EPC, scale, hw, lw);  // x chunk q holds source chunk q ^ h
       const int c16 = chunk_first + (q ^ h);
       // FP16 SW128: 16-byte chunk ^ row; TF32 SW128_BASE32B: 32-byte chunk ^ (row & 3)
       const uint32_t off = V == kFP16 ? base + ((c16 ^ rr) << 4)
                                       : base + ((((c16 >> 1) ^ rr) & 3) << 5) + ((c16 & 1) << 4);
-      sm100::sts128(hi_base + off, hw[4 * q], hw[4 * q + 1], hw[4 * q + 2], hw[4 * q + 3]);
-      sm100::sts128(lo_base + off, lw[4 * q], lw[4 * q + 1], lw[4 * q + 2], lw[4 * q + 3]);
+      sm100::sts128(hi_base + off, hw[0], hw[1], hw[2], hw[3]);
+      sm100::sts128(lo_base + off, lw[0], lw[1], lw[2], lw[3]);
     }
   }
 }
@@ -383,6 +383,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
       constexpr uint32_t b_lbo_w = (uint32_t(C::B_LBO) >> 4) << 16;
       constexpr uint32_t kB = C::B_KSTEP_BYTES >> 4;
       uint32_t git = 0;
+      int pos = 0;
       for (int kb = 0; kb < nop; ++kb) {
         const int o = kb % C::NOP;
         sm100::mbar_wait_cluster(&op_full[o], (kb / C::NOP) & 1);
@@ -393,7 +394,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
         const uint32_t bhi = (op + ((2 * C::OP_A_BYTES) >> 4)) | b_lbo_w;
         const uint32_t blo = bhi + (C::OP_B_BYTES >> 4);
         c3_stage(
-            kb * 4, 4 * nop, de, git, p_empty, p_full,
+            kb * 4, 4 * nop, de, pos, git, p_empty, p_full, &op_empty[o],
             [&](int ks) {  // reference order per k-step: dA*B_hi, then A_hi*dB
               sm100::mma_pair_split<V == kTF32>(tmem_dC, alo + 2 * ks, a_hi_w, bhi + kB * ks,
                                                 b_hi_w, idesc, (kb | ks) != 0);
@@ -404,7 +405,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
               sm100::mma_pair_split<V == kTF32>(tmem_P, ahi + 2 * ks, a_hi_w, bhi + kB * ks, b_hi_w,
                                                 idesc, acc);
             });
-        sm100::mma_commit_pair_mc(&op_empty[o], 0x3);
       }
     }
   } else if (warp < C::DRAIN_WARP0) {

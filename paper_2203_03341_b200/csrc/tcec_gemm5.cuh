@@ -199,6 +199,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
       constexpr uint32_t b_lbo_w = (uint32_t(C::B_LBO) >> 4) << 16;
       constexpr uint32_t kB = C::B_KSTEP_BYTES >> 4;
       uint32_t g = 0, git = 0, gtile = 0;
+      int pos = 0;
       for (int u = pid; u < num_units; u += npairs, ++gtile) {
         int tile, part, kb0, kb1;
         unit_of(u, tile, part, kb0, kb1);
@@ -217,7 +218,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
           const uint32_t bhi = (op + ((2 * C::OP_A_BYTES) >> 4)) | b_lbo_w;
           const uint32_t blo = bhi + (C::OP_B_BYTES >> 4);
           c3_stage(
-              kb * 4, 4 * nop_u, de, git, p_empty, p_full,
+              kb * 4, 4 * nop_u, de, pos, git, p_empty, p_full, &op_empty[o],
               [&](int ks) {  // schemes.py:294-298: dA*B_hi, then A_hi*dB
                 sm100::mma_pair_split<V == kTF32>(tmem_dC, alo + 2 * ks, a_hi_w, bhi + kB * ks,
                                                   b_hi_w, idesc, (kb | ks) != 0);
@@ -228,7 +229,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
                 sm100::mma_pair_split<V == kTF32>(tmem_P, ahi + 2 * ks, a_hi_w, bhi + kB * ks,
                                                   b_hi_w, idesc, acc);
               });
-          sm100::mma_commit_pair_mc(&op_empty[o], 0x3);
         }
       }
     }

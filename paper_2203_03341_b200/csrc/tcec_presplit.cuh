@@ -308,6 +308,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PsCfg<V, S>::NUM_THR
       constexpr uint32_t idesc = sm100::umma_idesc(VC::AB_FORMAT, 2 * C::BM, C::BN);
       constexpr uint32_t hi_w = (1024u >> 4) | (1u << 14) | (2u << 29);  // SBO 1024, v1, SW128
       uint32_t g = 0, git = 0, gtile = 0;
+      int pos = 0;  // k-steps into the current drain interval (corrected3)
       for (int tile = pid; tile < num_tiles; tile += npairs, ++gtile) {
         for (int kb = 0; kb < nop; ++kb, ++g) {
           const int o = g % C::NOP;
@@ -364,7 +365,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PsCfg<V, S>::NUM_THR
             }
           } else {
             c3_stage(
-                kb * 4, 4 * nop, de, git, p_empty, p_full,
+                kb * 4, 4 * nop, de, pos, git, p_empty, p_full, &op_empty[o],
                 [&](int ks) {  // reference order per k-step: dA*B then A*dB (schemes.py:294-298)
                   sm100::mma_pair_split<V == kTF32>(tmem_dC, alo + 2 * ks, hi_w, bhi + 2 * ks, hi_w,
                                                     idesc, (kb | ks) != 0);
@@ -379,7 +380,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PsCfg<V, S>::NUM_THR
                                                     idesc, acc);
                 });
           }
-          sm100::mma_commit_pair_mc(&op_empty[o], 0x3);
+          if constexpr (!C::kDrain)  // (c3_stage commits op_empty itself)
+            sm100::mma_commit_pair_mc(&op_empty[o], 0x3);
           if ((S == kSchPlain || S == kSchIn4) && kb == nop - 1) {
             sm100::mma_commit_pair_mc(p_full, 0x3);
             ++git;

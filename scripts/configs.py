@@ -8,6 +8,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
 import paper_2203_03341_b200 as T
+from bench import device_matrix
 from oracle import oracle as O
 
 torch.backends.cuda.matmul.allow_tf32 = False
@@ -41,7 +42,9 @@ def timed(fn, iters=3, warm=2):
 
 # ---- config 1: FP16-TCEC 1024^3 urand(-1,1), seeds 0..7 (+ TF32, cuBLAS SGEMM, oracle seed 0)
 if not only or "1" in only:
-    rows = {"fp16": [], "tf32": [], "sgemm": []}
+    rows = {"fp16": [], "fp16_block16": [], "tf32": [], "sgemm": [], "reference": []}
+    exact = 0
+    t_ref = 0.0
     for seed in range(8):
         a = O.urand(1024, 1024, -1, 1, seed)
         b = O.urand(1024, 1024, -1, 1, O.pair_seed(seed))
@@ -49,39 +52,57 @@ if not only or "1" in only:
         ref = A.double() @ B.double()
         for v in ("fp16", "tf32"):
             rows[v].append(relres(T.gemm_device(A, B, SCH[v]), ref))
+        c16 = T.gemm(A, B, SCH["fp16"], T.MmaConfig(block_k=16)).output  # the reference's schedule
+        rows["fp16_block16"].append(relres(c16, ref))
+        exact += int(np.array_equal(c16.cpu().numpy(), O.corrected3_hw(a, b, "fp16", drain_k=16)[0]))
         rows["sgemm"].append(relres(A @ B, ref))
-    t0 = time.time()
-    a = O.urand(1024, 1024, -1, 1, 0); b = O.urand(1024, 1024, -1, 1, O.pair_seed(0))
-    oc, _ = O.corrected3(a, b, "fp16", block_k=16, drain_k=16)   # the reference's own schedule
-    ref0 = torch.from_numpy(a).double() @ torch.from_numpy(b).double()
-    oracle_rel = float(torch.linalg.norm(ref0 - torch.from_numpy(oc).double()) / torch.linalg.norm(ref0))
-    emit({"config": 1, "desc": "FP16-TCEC 1024^3 urand(-1,1), relres vs FP64, seeds 0..7",
-          "relres_fp16_tcec_mean": float(np.mean(rows["fp16"])), "relres_tf32_tcec_mean": float(np.mean(rows["tf32"])),
-          "relres_cublas_sgemm_mean": float(np.mean(rows["sgemm"])), "per_seed_fp16": rows["fp16"],
-          "reference_algorithm_seed0_relres": oracle_rel, "reference_algorithm_seed0_cpu_s": time.time() - t0})
+        t0 = time.time()
+        oc, _ = O.corrected3(a, b, "fp16", block_k=16, drain_k=16)   # the reference's algorithm
+        t_ref += time.time() - t0
+        rows["reference"].append(relres(torch.from_numpy(oc).to(dev), ref))
+    emit({"config": 1, "desc": "FP16-TCEC 1024^3 urand(-1,1), relres vs FP64, seeds 0..7 (means)",
+          "relres_fp16_tcec_mean": float(np.mean(rows["fp16"])),
+          "relres_fp16_tcec_block_k16_mean": float(np.mean(rows["fp16_block16"])),
+          "relres_tf32_tcec_mean": float(np.mean(rows["tf32"])),
+          "relres_cublas_sgemm_mean": float(np.mean(rows["sgemm"])),
+          "relres_reference_algorithm_mean": float(np.mean(rows["reference"])),
+          "block_k16_bit_exact_vs_hw_oracle_seeds": exact,
+          "per_seed_fp16": rows["fp16"], "per_seed_reference": rows["reference"],
+          "reference_algorithm_cpu_s_total": t_ref, "host_threads": os.cpu_count()})
 
-# ---- config 2: square sweep 1024..16384, TF32-TCEC and FP16-TCEC vs cuBLAS SGEMM
+# ---- config 2: square sweep 1024..16384, TF32-TCEC and FP16-TCEC vs cuBLAS SGEMM, on
+# the config's full-FP32-exponent-range inputs ExpRand(-50, 50) (a_max + b_max +
+# log2 k < 127: no FP32 overflow), on urand(-1, 1), and for FP16-TCEC on its
+# in-range band ExpRand(-15, 14) (ExpRand(-50, 50) is outside the FP16 split's
+# range by design: flagged out_of_range / overflow, as the reference does)
 if not only or "2" in only:
     for n in (1024, 2048, 4096, 8192, 16384):
-        g = torch.Generator(device=dev); g.manual_seed(n)
-        A = torch.rand((n, n), generator=g, device=dev) * 2 - 1
-        B = torch.rand((n, n), generator=g, device=dev) * 2 - 1
-        C = torch.empty((n, n), device=dev)
-        rows_idx = torch.arange(0, n, max(1, n // 256), device=dev)
-        ref = A[rows_idx].double() @ B.double()
-        out = {"config": 2, "n": n}
-        for v in ("tf32", "fp16"):
-            ms = timed(lambda: T.gemm_device(A, B, SCH[v], out=C), iters=5 if n <= 8192 else 3)
-            out[f"{v}_tcec_tflops"] = 2 * n ** 3 / ms / 1e9
-            out[f"{v}_relres"] = relres(C[rows_idx], ref)
-            ms = timed(lambda: T.gemm_device(A, B, SCH[v], out=C, split_mode=2), iters=5 if n <= 8192 else 3)
-            out[f"{v}_tcec_split_once_tflops"] = 2 * n ** 3 / ms / 1e9
-        ms = timed(lambda: torch.matmul(A, B, out=C), iters=3)
-        out["cublas_sgemm_tflops"] = 2 * n ** 3 / ms / 1e9
-        out["cublas_sgemm_relres"] = relres(C[rows_idx], ref)
-        emit(out)
-        del A, B, C, ref
-        torch.cuda.empty_cache()
+        for dist in (("exprand", -50, 50), ("urand",), ("exprand", -15, 14)):
+            g = torch.Generator(device=dev); g.manual_seed(n)
+            A = device_matrix(dist, n, n, g, dev)
+            B = device_matrix(dist, n, n, g, dev)
+            C = torch.empty((n, n), device=dev)
+            rows_idx = torch.arange(0, n, max(1, n // 256), device=dev)
+            ref = A[rows_idx].double() @ B.double()
+            out = {"config": 2, "n": n, "dist": "urand(-1,1)" if dist[0] == "urand"
+                   else f"ExpRand({dist[1]},{dist[2]})"}
+            for v in ("tf32", "fp16"):
+                fl = torch.zeros(1, dtype=torch.int32, device=dev)
+                T.gemm_device(A, B, SCH[v], out=C, flags=fl)
+                out[f"{v}_flags"] = int(fl.item())
+                out[f"{v}_relres"] = relres(C[rows_idx], ref)
+                ms = timed(lambda: T.gemm_device(A, B, SCH[v], out=C), iters=5 if n <= 8192 else 3)
+                out[f"{v}_tcec_tflops"] = 2 * n ** 3 / ms / 1e9
+                if dist[0] == "urand":
+                    ms = timed(lambda: T.gemm_device(A, B, SCH[v], out=C, split_mode=2),
+                               iters=5 if n <= 8192 else 3)
+                    out[f"{v}_tcec_split_once_tflops"] = 2 * n ** 3 / ms / 1e9
+            ms = timed(lambda: torch.matmul(A, B, out=C), iters=3)
+            out["cublas_sgemm_tflops"] = 2 * n ** 3 / ms / 1e9
+            out["cublas_sgemm_relres"] = relres(C[rows_idx], ref)
+            emit(out)
+            del A, B, C, ref
+            torch.cuda.empty_cache()
 
 # ---- config 3: FP16-TCEC exponent sweep: ExpRand(e, e) for e in -15..15 and ExpRand(-15, 15)
 if not only or "3" in only:
