@@ -115,8 +115,11 @@ typedef struct tcec_opts {
   /* Kernel: 0 = automatic (persistent with lock-step waves for products of
    * >= 8 waves of 256 x 256 tiles, else per-tile); 1 = the single-CTA kernel
    * (block_n 128 only); 2 = persistent; 3 = persistent with lock-step waves;
-   * 4 = per-tile (for a kernel sharing the GPU with other work).  Results are
-   * bit-identical across kernels. */
+   * 4 = per-tile (for a kernel sharing the GPU with other work); 6 =
+   * persistent with the split shared through an L2-resident ring (each wave's
+   * A / B k-slices split once by the whole grid; corrected3, block_n 256, fused
+   * split; needs every SM -- not for a GPU shared with other kernels).
+   * Results are bit-identical across kernels. */
   int32_t kernel_variant;
   int32_t reserved[2];
 } tcec_opts;

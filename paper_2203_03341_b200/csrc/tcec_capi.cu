@@ -4,6 +4,7 @@
 // :327-330): shape errors are reported, numerical anomalies only raise flags.
 // Tensor maps are encoded per call through the driver entry point obtained
 // from the runtime (no link-time libcuda dependency).
+#include <algorithm>
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -22,6 +23,7 @@
 #include "tcec_gemm4.cuh"
 #include "tcec_gemm5.cuh"
 #include "tcec_presplit.cuh"
+#include "tcec_ring.cuh"
 #include "tcec_census.cuh"
 
 namespace {
@@ -313,6 +315,112 @@ int launch_gemm_presplit(int64_t m, int64_t n, int64_t k, const float* A, int64_
   return st;
 }
 
+// Fused GEMM with the split shared through an L2-resident ring (kernel_variant
+// 6, tcec_ring.cuh): every CTA of a co-resident persistent grid splits its
+// share of each wave's k-slices once; the pairs TMA the split operands.
+template <int V, int R>
+int launch_gemm_ring(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, const float* B,
+                     int64_t ldb, float* C, int64_t ldc, int scale_log2, int drain_every,
+                     int group_m, uint32_t* d_flags, cudaStream_t stream) {
+  using Cfg = tcec::PsCfg<V, tcec::kSchC3>;
+  using VC = tcec::VarCfg<V>;
+  const uint32_t esize = V == tcec::kFP16 ? 2u : 4u;
+  const CUtensorMapDataType dt =
+      V == tcec::kFP16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return TCEC_ERR_CUDA;
+  auto kern = tcec::tcec_gemm_ring_kernel<V, R>;
+  if (smem_optin(kern, tcec::ring_smem_bytes<V>()) != cudaSuccess) return TCEC_ERR_CUDA;
+  // every CTA splits: the grid must be co-resident (one pair per TPC)
+  static std::mutex occ_mu;
+  static int occ_pairs[64] = {0};
+  int max_pairs = 0;
+  {
+    std::lock_guard<std::mutex> lk(occ_mu);
+    if (dev >= 0 && dev < 64 && occ_pairs[dev] == 0) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(2, 1, 1);
+      cfg.blockDim = dim3(640, 1, 1);
+      cfg.dynamicSmemBytes = tcec::ring_smem_bytes<V>();
+      if (cudaOccupancyMaxActiveClusters(&occ_pairs[dev], kern, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        occ_pairs[dev] = -1;
+      }
+    }
+    if (dev >= 0 && dev < 64) max_pairs = occ_pairs[dev];
+  }
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int np = sms / 2;
+  if (max_pairs > 0 && max_pairs < np) np = max_pairs;
+  const int tiles_m = static_cast<int>((m + 255) / 256), tiles_n = static_cast<int>((n + 255) / 256);
+  const int tiles = tiles_m * tiles_n;
+  if (np > tiles) np = tiles;
+  if (np < 1) return TCEC_ERR_CUDA;
+  const int gm = group_m > 0 ? group_m : 8;
+  const int waves = (tiles + np - 1) / np;
+  const int nop = static_cast<int>((k + VC::BK_OP - 1) / VC::BK_OP);
+  int la_max = 1, lb_max = 1;
+  for (int w = 0; w < waves; ++w) {
+    const tcec::RingWave rw = tcec::ring_wave(w, np, tiles, tiles_m, tiles_n, gm);
+    la_max = std::max(la_max, rw.la);
+    lb_max = std::max(lb_max, rw.lb);
+  }
+  // ring depth in slices: 16 covers the split -> release -> TMA chain
+  // (8: FP16 331, 12: 361, 16-32: 364-368 TF/s at 16384^3, profiles/r02/ring.md)
+  const int depth = 16;
+  const size_t slot_rows_a = size_t(la_max) * 256, slot_rows_b = size_t(lb_max) * 256;
+  const size_t ring_a = depth * slot_rows_a * 128, ring_b = depth * slot_rows_b * 128;
+  const size_t slices = size_t(waves) * nop;
+  const size_t ctr_bytes = slices * (la_max + lb_max + 1) * sizeof(uint32_t);
+  keep_pool(dev);
+  uint8_t* ws = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&ws), 2 * (ring_a + ring_b) + ctr_bytes, stream) !=
+      cudaSuccess)
+    return TCEC_ERR_CUDA;
+  tcec::RingArgs ra;
+  ra.A = A;
+  ra.B = B;
+  ra.lda = lda;
+  ra.ldb = ldb;
+  ra.ahi = ws;
+  ra.alo = ws + ring_a;
+  ra.bhi = ws + 2 * ring_a;
+  ra.blo = ws + 2 * ring_a + ring_b;
+  ra.ready = reinterpret_cast<uint32_t*>(ws + 2 * (ring_a + ring_b));
+  ra.freed = ra.ready + slices * (la_max + lb_max);
+  ra.depth = depth;
+  ra.la_max = la_max;
+  ra.lb_max = lb_max;
+  ra.np = np;
+  int st = TCEC_OK;
+  CUtensorMap tmAh, tmAl, tmBh, tmBl;
+  const uint64_t bk = VC::BK_OP;
+  if (!st) st = make_tmap_op(&tmAh, ra.ahi, dt, esize, bk, depth * slot_rows_a, bk, Cfg::BM);
+  if (!st) st = make_tmap_op(&tmAl, ra.alo, dt, esize, bk, depth * slot_rows_a, bk, Cfg::BM);
+  if (!st) st = make_tmap_op(&tmBh, ra.bhi, dt, esize, bk, depth * slot_rows_b, bk, Cfg::BN_CTA);
+  if (!st) st = make_tmap_op(&tmBl, ra.blo, dt, esize, bk, depth * slot_rows_b, bk, Cfg::BN_CTA);
+  if (!st && cudaMemsetAsync(ra.ready, 0, ctr_bytes, stream) != cudaSuccess) st = TCEC_ERR_CUDA;
+  if (!st) {
+    tcec::GemmShape shp;
+    shp.m = static_cast<int32_t>(m);
+    shp.n = static_cast<int32_t>(n);
+    shp.k = static_cast<int32_t>(k);
+    shp.num_op_stages = nop;
+    shp.drain_every = drain_every;
+    shp.group_m = gm;
+    const float scale = ldexpf(1.0f, scale_log2);
+    const float inv_scale = ldexpf(1.0f, -scale_log2);
+    const tcec::FlagThresholds thr = tcec::flag_thresholds(V, R, scale_log2);
+    kern<<<static_cast<unsigned>(2 * np), 640, tcec::ring_smem_bytes<V>(), stream>>>(
+        tmAh, tmAl, tmBh, tmBl, C, ldc, shp, ra, scale, inv_scale, thr, d_flags);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (cudaGetLastError() != cudaSuccess) st = TCEC_ERR_CUDA;
+  }
+  cudaFreeAsync(ws, stream);
+  return st;
+}
+
 // Persistent CTA-pair kernel (kernel_variant 2): one pair per TPC walks the
 // tile sequence with its pipelines running across tiles.
 template <int V, int R>
@@ -456,6 +564,10 @@ int dispatch(const Plan& p, int64_t m, int64_t n, int64_t k, const float* A, int
     }
   }
   if (p.block_n == 256) {
+    if (kv == 6) {  // split shared through the L2-resident ring
+      const int g = p.group_user > 0 ? gpair : 8;
+      return launch_gemm_ring<V, R>(m, n, k, A, lda, B, ldb, C, ldc, s, de, g, fl, st);
+    }
     if (kv == 2 || kv == 3) {  // persistent; 3 = with lock-step waves
       const int g = p.group_user > 0 ? gpair : (kv == 3 ? 8 : 4);
       return launch_gemm_pers<V, R>(m, n, k, A, lda, B, ldb, C, ldc, s, de, g, kv == 3, fl, st);
@@ -634,9 +746,11 @@ int sgemm_impl(int variant, int64_t m, int64_t n, int64_t k, const float* A, int
   p.group_user = o.group_m;
   p.group_m = o.group_m <= 0 ? 8 : o.group_m;
   // kernel_variant: 0 = automatic, 1 = single-CTA (block_n 128), 2 = persistent,
-  // 3 = persistent with lock-step waves, 4 = per-tile
+  // 3 = persistent with lock-step waves, 4 = per-tile, 6 = persistent with the
+  // split shared through an L2-resident ring (tcec_ring.cuh)
   p.kvariant = p.kv_user = o.kernel_variant;
-  if (p.kvariant < 0 || p.kvariant > 4) return TCEC_ERR_UNSUPPORTED;
+  if (p.kvariant < 0 || p.kvariant > 6 || p.kvariant == 5) return TCEC_ERR_UNSUPPORTED;
+  if (p.kvariant == 6 && (o.block_n != 0 && o.block_n != 256)) return TCEC_ERR_UNSUPPORTED;
   if (p.kvariant == 1 && o.block_n != 128) return TCEC_ERR_UNSUPPORTED;
   // split_mode: 0 / 1 = split fused into the GEMM, 2 = split once in a separate pass
   p.split_mode = o.split_mode;

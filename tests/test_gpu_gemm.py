@@ -428,7 +428,7 @@ def test_pair_kernel_bitwise_equals_single_cta_kernel(sname, variant, bk, drain,
 
 OPTION_SETS = [{"block_n": 128}, {"block_n": 128, "kernel_variant": 1}, {"block_n": 192},
                {"block_n": 256}, {"split_mode": 2}, {"kernel_variant": 2}, {"kernel_variant": 3},
-               {"kernel_variant": 4}]
+               {"kernel_variant": 4}, {"kernel_variant": 6}]
 
 
 @pytest.mark.parametrize("opts", OPTION_SETS, ids=lambda o: ",".join(f"{k}={v}" for k, v in o.items()))
@@ -462,6 +462,38 @@ def test_kernel_options_bitwise_equal(sname, variant, bk, drain, shape, opts):
         c1 = T.gemm_device(A, B, sname, flags=f1, **opts)
         assert torch.equal(c0.view(torch.int32), c1.view(torch.int32)), (opts, wide)
         assert int(f0.item()) == int(f1.item()), (opts, wide)
+
+
+@pytest.mark.parametrize("drain_k", [0, 16, 48])
+@pytest.mark.parametrize("sname", ["corrected3_halfhalf", "corrected3_tf32"])
+@pytest.mark.parametrize("shape", [(4096, 4096, 1024), (2560, 3000, 777), (16384, 1024, 300),
+                                   (1024, 20000, 200), (8192, 8192, 640)])
+def test_ring_kernel_bitwise_equal(sname, shape, drain_k):
+    """kernel_variant 6 (the split shared through the L2 ring, tcec_ring.cuh):
+    many waves of 74 tiles, waves straddling raster groups, few columns of tiles
+    (several groups per wave), ragged edges, a drain interval that is not a
+    whole operand stage, and one row / column whose hi overflows -- C and
+    RunFlags bit-identical to the per-tile fused kernel."""
+    import torch
+
+    T = _T()
+    m, n, k = shape
+    if drain_k and sname == "corrected3_tf32":
+        drain_k //= 2
+    g = torch.Generator(device="cuda")
+    g.manual_seed(m + 3 * n + 7 * k)
+    A = torch.rand((m, k), generator=g, device="cuda") * 2 - 1
+    B = torch.rand((k, n), generator=g, device="cuda") * 2 - 1
+    A[m // 3] *= 2.0 ** 16
+    B[:, n - 5] *= 2.0 ** 17
+    f0 = torch.zeros(1, dtype=torch.int32, device="cuda")
+    f6 = torch.zeros(1, dtype=torch.int32, device="cuda")
+    c0 = T.gemm_device(A, B, sname, flags=f0, kernel_variant=4, drain_k=drain_k)
+    c6 = T.gemm_device(A, B, sname, flags=f6, kernel_variant=6, drain_k=drain_k)
+    assert torch.equal(c0.view(torch.int32), c6.view(torch.int32))
+    assert int(f0.item()) == int(f6.item())
+    if sname == "corrected3_halfhalf":
+        assert int(f0.item()) & 1  # hi overflowed
 
 
 @pytest.mark.parametrize("sname", ["corrected3_halfhalf", "corrected3_tf32"])
