@@ -118,7 +118,9 @@ typedef struct tcec_opts {
    * 4 = per-tile (for a kernel sharing the GPU with other work); 6 =
    * persistent with the split shared through an L2-resident ring (each wave's
    * A / B k-slices split once by the whole grid; corrected3, block_n 256, fused
-   * split; needs every SM -- not for a GPU shared with other kernels).
+   * split; needs every SM -- not for a GPU shared with other kernels; measured
+   * slower than the default, so only in libraries built with `make RING=1`,
+   * TCEC_ERR_UNSUPPORTED otherwise).
    * Results are bit-identical across kernels. */
   int32_t kernel_variant;
   int32_t reserved[2];

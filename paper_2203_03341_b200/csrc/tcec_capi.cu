@@ -23,7 +23,9 @@
 #include "tcec_gemm4.cuh"
 #include "tcec_gemm5.cuh"
 #include "tcec_presplit.cuh"
+#ifdef TCEC_WITH_RING  // kernel_variant 6, measured slower: built with `make RING=1` only
 #include "tcec_ring.cuh"
+#endif
 #include "tcec_census.cuh"
 
 namespace {
@@ -315,6 +317,7 @@ int launch_gemm_presplit(int64_t m, int64_t n, int64_t k, const float* A, int64_
   return st;
 }
 
+#ifdef TCEC_WITH_RING
 // Fused GEMM with the split shared through an L2-resident ring (kernel_variant
 // 6, tcec_ring.cuh): every CTA of a co-resident persistent grid splits its
 // share of each wave's k-slices once; the pairs TMA the split operands.
@@ -420,6 +423,7 @@ int launch_gemm_ring(int64_t m, int64_t n, int64_t k, const float* A, int64_t ld
   cudaFreeAsync(ws, stream);
   return st;
 }
+#endif  // TCEC_WITH_RING
 
 // Persistent CTA-pair kernel (kernel_variant 2): one pair per TPC walks the
 // tile sequence with its pipelines running across tiles.
@@ -565,8 +569,12 @@ int dispatch(const Plan& p, int64_t m, int64_t n, int64_t k, const float* A, int
   }
   if (p.block_n == 256) {
     if (kv == 6) {  // split shared through the L2-resident ring
+#ifdef TCEC_WITH_RING
       const int g = p.group_user > 0 ? gpair : 8;
       return launch_gemm_ring<V, R>(m, n, k, A, lda, B, ldb, C, ldc, s, de, g, fl, st);
+#else
+      return TCEC_ERR_UNSUPPORTED;
+#endif
     }
     if (kv == 2 || kv == 3) {  // persistent; 3 = with lock-step waves
       const int g = p.group_user > 0 ? gpair : (kv == 3 ? 8 : 4);
