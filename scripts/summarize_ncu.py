@@ -18,7 +18,7 @@ out_path = sys.argv[1]
 for rep in sys.argv[2:]:
     d = raw(rep)
     name = os.path.basename(rep).replace(".ncu-rep", "")
-    variant = "tf32" if "tf32" in name else "fp16"
+    variant = ("tf32" if "tf32" in name else "fp16") + ("_split_once" if "splitonce" in name else "")
     t = num(d, "gpu__time_duration.sum")
     rd = num(d, "dram__bytes_read.sum")
     wr = num(d, "dram__bytes_write.sum")
