@@ -1,3 +1,6 @@
+"""e2e through tcec_sgemm_host by blocking and number of compute streams (TCEC_NSC).
+Needs a measurement build with HostCtx::kMaxBlk = 16 and four compute streams
+(profiles/r02/e2e/README.md); the library clamps blocks to 8 and uses two."""
 import ctypes, os, sys, time
 sys.path.insert(0, os.getcwd())
 import torch
