@@ -83,10 +83,10 @@ typedef struct tcec_opts {
    * TCEC_SCHEME_INUNIT4_RN: the block of each drained product (see above). */
   int32_t drain_k;
   /* Output tile width: 0 = automatic (the CTA-pair 256 x 256 tile, or below
-   * 8 waves of those the width among 256 / 192 / 128 with the fewest
-   * cost-weighted waves; same results); 192 / 128 = CTA-pair 256 x 192 / 256 x 128 tile with the
-   * split A operand in tensor memory (128 with kernel_variant = 1: the
-   * single-CTA 128 x 128 kernel). */
+   * 8 waves of those the width among 256 / 192 / 128 / 64 with the fewest
+   * cost-weighted waves; same results); 192 / 128 / 64 = CTA-pair 256 x 192 /
+   * 256 x 128 / 256 x 64 tile with the split A operand in tensor memory (128
+   * with kernel_variant = 1: the single-CTA 128 x 128 kernel). */
   int32_t block_n;
   /* Tile rasterisation group along m in 128-row tiles: 0 = default (8). */
   int32_t group_m;

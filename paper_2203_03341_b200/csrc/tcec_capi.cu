@@ -596,6 +596,10 @@ int dispatch(const Plan& p, int64_t m, int64_t n, int64_t k, const float* A, int
     if (kv != 4) return TCEC_ERR_UNSUPPORTED;
     return launch_gemm_ts<V, R, 128, 4>(m, n, k, A, lda, B, ldb, C, ldc, s, de, gpair, fl, st);
   }
+  if (p.block_n == 64) {  // 256 x 64: small products, more CTA pairs busy
+    if (kv != 4) return TCEC_ERR_UNSUPPORTED;
+    return launch_gemm_ts<V, R, 64, 4>(m, n, k, A, lda, B, ldb, C, ldc, s, de, gpair, fl, st);
+  }
   return TCEC_ERR_UNSUPPORTED;
 }
 
@@ -747,10 +751,12 @@ int sgemm_impl(int variant, int64_t m, int64_t n, int64_t k, const float* A, int
                                      : (o.scheme == TCEC_SCHEME_INUNIT4_RN ? 16 : 8 * kstep);
   if (drain_k <= 0 || drain_k % kstep != 0) return TCEC_ERR_UNSUPPORTED;
   p.drain_every = drain_k / kstep;
-  if (o.block_n != 0 && o.block_n != 128 && o.block_n != 192 && o.block_n != 256)
+  if (o.block_n != 0 && o.block_n != 64 && o.block_n != 128 && o.block_n != 192 &&
+      o.block_n != 256)
     return TCEC_ERR_UNSUPPORTED;
   // the narrow tiles drain whole operand stages (4 k-steps)
-  if ((o.block_n == 128 || o.block_n == 192) && p.drain_every % 4 != 0) return TCEC_ERR_UNSUPPORTED;
+  if ((o.block_n == 64 || o.block_n == 128 || o.block_n == 192) && p.drain_every % 4 != 0)
+    return TCEC_ERR_UNSUPPORTED;
   p.group_user = o.group_m;
   p.group_m = o.group_m <= 0 ? 8 : o.group_m;
   // kernel_variant: 0 = automatic, 1 = single-CTA (block_n 128), 2 = persistent,
@@ -786,18 +792,20 @@ int sgemm_impl(int variant, int64_t m, int64_t n, int64_t k, const float* A, int
     // automatic tile.  Below 8 waves of 256 x 256 tiles (the persistent
     // kernel's range) the per-tile kernels are wave-quantised: pick the width
     // minimising waves x width x per-flop cost, with the narrow A-from-TMEM
-    // tiles' measured costs 1.1 (256 x 192) and 1.25 (256 x 128) -- 1024^2 and
-    // 1536^2 take 128, 1792^2 and 2560^2 take 192, 2048^2 and >= 3072^2 keep
-    // 256 (profiles/r01/smallbn.log, midbn.log).  Results are bit-identical.
+    // tiles' measured costs 1.1 (256 x 192), 1.25 (256 x 128) and 2.0 (256 x
+    // 64) -- products that fit one wave of 256 x 64 tiles (1024^2, 768^2,
+    // 512 x 1024) take 64, 1536^2 takes 128, 1792^2 and 2560^2 take 192, 2048^2
+    // and >= 3072^2 keep 256 (profiles/r01/smallbn.log, midbn.log,
+    // profiles/r02/smallbn_r02.jsonl).  Results are bit-identical.
     // The narrow tiles drain per operand stage (multiples of 4 k-steps).
     p.block_n = 256;
     if ((p.kvariant == 0 || p.kvariant == 4) && fused_c3 && ex == nullptr && p.split_k <= 1 &&
         p.drain_every % 4 == 0 && tiles256 < 8 * pairs) {
       const int64_t rows = (m + 255) / 256;
       double best = 0.0;
-      const int widths[3] = {256, 192, 128};
-      const double eff[3] = {1.0, 1.1, 1.25};
-      for (int i = 0; i < 3; ++i) {
+      const int widths[4] = {256, 192, 128, 64};
+      const double eff[4] = {1.0, 1.1, 1.25, 2.0};
+      for (int i = 0; i < 4; ++i) {
         const int64_t waves = (rows * ((n + widths[i] - 1) / widths[i]) + pairs - 1) / pairs;
         const double cost = double(waves) * widths[i] * eff[i];
         if (i == 0 || cost < best) {

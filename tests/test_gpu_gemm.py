@@ -449,7 +449,7 @@ def test_pair_kernel_bitwise_equals_single_cta_kernel(sname, variant, bk, drain,
     assert int(f1.item()) == int(f2.item()) == int(f3.item())
 
 
-OPTION_SETS = [{"block_n": 128}, {"block_n": 128, "kernel_variant": 1}, {"block_n": 192},
+OPTION_SETS = [{"block_n": 64}, {"block_n": 128}, {"block_n": 128, "kernel_variant": 1}, {"block_n": 192},
                {"block_n": 256}, {"split_mode": 2}, {"kernel_variant": 2}, {"kernel_variant": 3},
                {"kernel_variant": 4}, {"kernel_variant": 6}]
 
@@ -459,7 +459,7 @@ OPTION_SETS = [{"block_n": 128}, {"block_n": 128, "kernel_variant": 1}, {"block_
 @pytest.mark.parametrize("shape", [(256, 192, 64), (300, 200, 1000), (77, 1000, 130), (520, 576, 2048)])
 def test_kernel_options_bitwise_equal(sname, variant, bk, drain, shape, opts):
     """Every kernel option runs the default path's per-element arithmetic: the
-    A-from-TMEM pair kernels (block_n=192 / 128), the single-CTA kernel, the
+    A-from-TMEM pair kernels (block_n=192 / 128 / 64), the single-CTA kernel, the
     persistent / lock-step / per-tile pair kernels and the split-once mode
     (split_mode=2: separate split pass + three-product GEMM over pre-split
     operands) give bit-identical C and flags,
