@@ -414,6 +414,72 @@ __device__ __forceinline__ void mma_pair_ts(uint32_t d_tmem, uint32_t a_tmem, ui
   }
 }
 
+// Warp-converged issue: the whole MMA warp runs the issue loop (warp-uniform
+// descriptors, no per-instruction register -> uniform-register hand-off from a
+// divergent lane) and elect.sync picks the one lane that issues.
+template <bool kTF32>
+__device__ __forceinline__ void mma_pair_ts_el(uint32_t d_tmem, uint32_t a_tmem, uint32_t b_lo,
+                                               uint32_t b_hi, uint32_t idesc, uint32_t accumulate) {
+  if constexpr (kTF32) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p, e;\n"
+        ".reg .b64 bd;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "mov.b64 bd, {%2, %3};\n"
+        "setp.ne.b32 p, %5, 0;\n"
+        "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], bd, %4, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(accumulate)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n"
+        ".reg .pred p, e;\n"
+        ".reg .b64 bd;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "mov.b64 bd, {%2, %3};\n"
+        "setp.ne.b32 p, %5, 0;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], bd, %4, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(accumulate)
+        : "memory");
+  }
+}
+
+template <bool kTF32>
+__device__ __forceinline__ void mma_pair_split_el(uint32_t d_tmem, uint32_t a_lo, uint32_t a_hi,
+                                                  uint32_t b_lo, uint32_t b_hi, uint32_t idesc,
+                                                  uint32_t accumulate) {
+  if constexpr (kTF32) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p, e;\n"
+        ".reg .b64 ad, bd;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "mov.b64 ad, {%1, %2};\n"
+        "mov.b64 bd, {%3, %4};\n"
+        "setp.ne.b32 p, %6, 0;\n"
+        "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], ad, bd, %5, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(accumulate)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n"
+        ".reg .pred p, e;\n"
+        ".reg .b64 ad, bd;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "mov.b64 ad, {%1, %2};\n"
+        "mov.b64 bd, {%3, %4};\n"
+        "setp.ne.b32 p, %6, 0;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], ad, bd, %5, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(accumulate)
+        : "memory");
+  }
+}
+
 // 32 lanes x 8 / 16 consecutive 32-bit columns <- registers (one lane per thread).
 __device__ __forceinline__ void tmem_st_32x32b_x8(uint32_t taddr, const uint32_t* r) {
   asm volatile(
@@ -478,6 +544,19 @@ __device__ __forceinline__ void mma_commit_pair_mc(uint64_t* bar, uint16_t cta_m
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
       " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(cta_mask)
+      : "memory");
+}
+
+// Warp-converged form of mma_commit_pair_mc (one elected lane commits).
+__device__ __forceinline__ void mma_commit_pair_mc_el(uint64_t* bar, uint16_t cta_mask) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;\n"
+      "}\n" ::"r"(smem_u32(bar)),
       "h"(cta_mask)
       : "memory");
 }

@@ -594,7 +594,7 @@ int dispatch(const Plan& p, int64_t m, int64_t n, int64_t k, const float* A, int
     // first kernel); otherwise the CTA-pair 256 x 128 tile with A in TMEM
     if (kv == 1) return launch_gemm<V, R, 128>(m, n, k, A, lda, B, ldb, C, ldc, s, de, gm, fl, st);
     if (kv != 4) return TCEC_ERR_UNSUPPORTED;
-    return launch_gemm_ts<V, R, 128, 4>(m, n, k, A, lda, B, ldb, C, ldc, s, de, gpair, fl, st);
+    return launch_gemm_ts<V, R, 128, 2>(m, n, k, A, lda, B, ldb, C, ldc, s, de, gpair, fl, st);
   }
   if (p.block_n == 64) {  // 256 x 64: small products, more CTA pairs busy
     if (kv != 4) return TCEC_ERR_UNSUPPORTED;

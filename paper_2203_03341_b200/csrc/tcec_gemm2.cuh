@@ -62,7 +62,8 @@ struct PairCfg {
   static_assert(NUM_DRAIN_WARPS * EPI_WARP_BYTES <= OFF_BAR, "epilogue staging reuses the rings");
 };
 
-// The MMAs of one operand stage (4 MMA k-steps) of the corrected3 schedule.
+// The MMAs of one operand stage (4 MMA k-steps) of the corrected3 schedule,
+// issued by the whole (converged) MMA warp through elect.sync.
 // corr(ks) issues k-step ks's correction products into dC (schemes.py:294-298);
 // mainp(ks, acc) its main product into P.  P is drained every `de` k-steps --
 // the main-term block of schemes.py:300-304 with block_k = de x MMA-K: the
@@ -93,10 +94,10 @@ __device__ __forceinline__ void c3_stage(int j0, int nks, int de, int& pos, uint
     }
 #pragma unroll
     for (int ks = 0; ks < 4; ++ks) mainp(ks, (first && ks == 0) ? 0u : 1u);
-    sm100::mma_commit_pair_mc(op_empty, 0x3);
+    sm100::mma_commit_pair_mc_el(op_empty, 0x3);
     pos += 4;
     if (pos == de || j0 + 4 >= nks) {
-      sm100::mma_commit_pair_mc(p_full, 0x3);
+      sm100::mma_commit_pair_mc_el(p_full, 0x3);
       ++git;
       pos = 0;
     }
@@ -111,12 +112,12 @@ __device__ __forceinline__ void c3_stage(int j0, int nks, int de, int& pos, uint
     }
     mainp(ks, pos == 0 ? 0u : 1u);
     if (++pos == de || j0 + ks == nks - 1) {
-      sm100::mma_commit_pair_mc(p_full, 0x3);
+      sm100::mma_commit_pair_mc_el(p_full, 0x3);
       ++git;
       pos = 0;
     }
   }
-  sm100::mma_commit_pair_mc(op_empty, 0x3);
+  sm100::mma_commit_pair_mc_el(op_empty, 0x3);
 }
 
 // Split one 32-deep FP32 slice of this CTA's A rows and B columns into the
@@ -375,7 +376,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
           sm100::tma_load_2d(dst + C::STG_A_BYTES + b * C::STG_B_BOX, &tmB, &stg_full[s],
                              n_cta + 32 * b, st * C::BK_STG);
       }
-    } else if (warp == 1 && lane == 0 && rank == 0) {
+    } else if (warp == 1 && rank == 0) {  // the whole warp runs the issue loop; one elected lane issues
       // ===================== MMA issuer (leader CTA) =====================
       constexpr uint32_t idesc = sm100::umma_idesc_bmn(VC::AB_FORMAT, 2 * C::BM, C::BN);
       // descriptor high words: SBO | version 1 | layout (K-major A: SW128; MN-major B)
@@ -397,13 +398,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
         c3_stage(
             kb * 4, 4 * nop, de, pos, git, p_empty, p_full, &op_empty[o],
             [&](int ks) {  // reference order per k-step: dA*B_hi, then A_hi*dB
-              sm100::mma_pair_split<V == kTF32>(tmem_dC, alo + 2 * ks, a_hi_w, bhi + kB * ks,
+              sm100::mma_pair_split_el<V == kTF32>(tmem_dC, alo + 2 * ks, a_hi_w, bhi + kB * ks,
                                                 b_hi_w, idesc, (kb | ks) != 0);
-              sm100::mma_pair_split<V == kTF32>(tmem_dC, ahi + 2 * ks, a_hi_w, blo + kB * ks,
+              sm100::mma_pair_split_el<V == kTF32>(tmem_dC, ahi + 2 * ks, a_hi_w, blo + kB * ks,
                                                 b_hi_w, idesc, 1u);
             },
             [&](int ks, uint32_t acc) {
-              sm100::mma_pair_split<V == kTF32>(tmem_P, ahi + 2 * ks, a_hi_w, bhi + kB * ks, b_hi_w,
+              sm100::mma_pair_split_el<V == kTF32>(tmem_P, ahi + 2 * ks, a_hi_w, bhi + kB * ks, b_hi_w,
                                                 idesc, acc);
             });
       }

@@ -56,15 +56,22 @@ struct TsCfg {
   static constexpr int OFF_STG = 0;
   static constexpr int OFF_OP = NSTG * STG_BYTES;
   static constexpr int OFF_BAR = OFF_OP + NOP * OP_BYTES;
-  static constexpr int NUM_BARS = 2 * NSTG + 2 * NOP + 2;
-  static constexpr int SMEM_BYTES = OFF_BAR + NUM_BARS * 8 + 16;
-  // TMEM columns: P [0,192) | dC [192,384) | A ring [384,512): stage o at
-  // 384 + 64 o, A_hi in its first 32 columns and A_lo in the next 32 (8
-  // columns per MMA k-step: 16 FP16 packed in pairs, or 8 TF32).
+  // TMEM columns: P [0,BN) | dC [BN,2BN) | A ring [2BN, 2BN + 64 NOP): stage o
+  // at 2BN + 64 o, A_hi in its first 32 columns and A_lo in the next 32 (8
+  // columns per MMA k-step: 16 FP16 packed in pairs, or 8 TF32) | a second P
+  // buffer where the 512 columns leave room (256 x 64 with NOP 4, 256 x 128
+  // with NOP 2): the MMAs of drain interval j + 1 then start while the drain
+  // warps still read interval j's partial, which removes the per-interval
+  // drain round trip from the critical path of the narrow tiles (their MMAs
+  // are too short to hide it).
   static constexpr int TMEM_COLS = 512;
   static constexpr int T_DC = BN;
   static constexpr int T_A = 2 * BN;
   static constexpr int T_A_STAGE = 64;
+  static constexpr int T_P1 = T_A + NOP * T_A_STAGE;
+  static constexpr int NPB = T_P1 + BN <= TMEM_COLS ? 2 : 1;  // P buffers
+  static constexpr int NUM_BARS = 2 * NSTG + 2 * NOP + 2 * NPB;
+  static constexpr int SMEM_BYTES = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr int NUM_THREADS = 640;
   static constexpr int SPLIT_WARP0 = 4, NUM_SPLIT_WARPS = 8;
   static constexpr int DRAIN_WARP0 = 12, NUM_DRAIN_WARPS = 8;
@@ -205,8 +212,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
   uint64_t* stg_empty = bars + C::NSTG;         // split -> TMA          (local, 8)
   uint64_t* op_full = bars + 2 * C::NSTG;       // split -> MMA          (leader, 16)
   uint64_t* op_empty = op_full + C::NOP;        // MMA commit -> split   (both, multicast)
-  uint64_t* p_full = op_empty + C::NOP;         // MMA commit -> drain   (both, multicast)
-  uint64_t* p_empty = p_full + 1;               // drain -> MMA          (leader, 16)
+  uint64_t* p_full = op_empty + C::NOP;         // [NPB] MMA commit -> drain (both, multicast)
+  uint64_t* p_empty = p_full + C::NPB;          // [NPB] drain -> MMA        (leader, 16)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NUM_BARS);
   const uint32_t smem_base = sm100::smem_u32(smem);
 
@@ -249,8 +256,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
       sm100::mbar_init(&op_full[o], 2 * C::NUM_SPLIT_WARPS);
       sm100::mbar_init(&op_empty[o], 1);
     }
-    sm100::mbar_init(p_full, 1);
-    sm100::mbar_init(p_empty, 2 * C::NUM_DRAIN_WARPS);
+    for (int b = 0; b < C::NPB; ++b) {
+      sm100::mbar_init(&p_full[b], 1);
+      sm100::mbar_init(&p_empty[b], 2 * C::NUM_DRAIN_WARPS);
+    }
     sm100::fence_mbar_init();
   }
   if (warp == 2) sm100::tmem_alloc_pair<C::TMEM_COLS>(tmem_slot);
@@ -260,6 +269,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
   const uint32_t tmem_base = *tmem_slot;
   const uint32_t tmem_P = tmem_base;
   const uint32_t tmem_dC = tmem_base + C::T_DC;
+  // P buffer of drain interval j: j % NPB
+  auto p_buf = [&](int j) { return (C::NPB == 2 && (j & 1)) ? tmem_base + C::T_P1 : tmem_P; };
 
   if (warp < 4) {
     sm100::regs_dec<40>();
@@ -276,8 +287,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
           sm100::tma_load_2d(dst + C::STG_A_BYTES + b * C::STG_B_BOX, &tmB, &stg_full[s],
                              n_cta + 32 * b, st * C::BK_STG);
       }
-    } else if (warp == 1 && lane == 0 && rank == 0) {
-      // ===================== MMA issuer (leader CTA) =====================
+    } else if (warp == 1 && rank == 0) {
+      // ===================== MMA issuer (leader CTA; the whole warp runs the loop,
+      // one elected lane issues) =====================
       constexpr uint32_t idesc = sm100::umma_idesc_bmn(VC::AB_FORMAT, 2 * C::BM, C::BN);
       constexpr uint32_t b_hi_w = (uint32_t(C::B_SBO) >> 4) | (1u << 14) | (C::B_LAYOUT << 29);
       constexpr uint32_t b_lbo_w = (uint32_t(C::B_LBO) >> 4) << 16;
@@ -295,22 +307,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
         // drain of the previous P overlaps them (schemes.py:294-298)
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {
-          sm100::mma_pair_ts<V == kTF32>(tmem_dC, alo + 8 * ks, bhi + kB * ks, b_hi_w, idesc,
+          sm100::mma_pair_ts_el<V == kTF32>(tmem_dC, alo + 8 * ks, bhi + kB * ks, b_hi_w, idesc,
                                          (kb | ks) != 0);
-          sm100::mma_pair_ts<V == kTF32>(tmem_dC, ahi + 8 * ks, blo + kB * ks, b_hi_w, idesc, 1u);
+          sm100::mma_pair_ts_el<V == kTF32>(tmem_dC, ahi + 8 * ks, blo + kB * ks, b_hi_w, idesc, 1u);
         }
         const bool first_in_interval = (kb % de) == 0;
-        if (first_in_interval && kb > 0) {
-          sm100::mbar_wait_cluster(p_empty, ((kb / de) - 1) & 1);
+        const int j = kb / de;  // drain interval
+        const int b = j % C::NPB;
+        if (first_in_interval && j >= C::NPB) {  // the drain of interval j - NPB has read buffer b
+          sm100::mbar_wait_cluster(&p_empty[b], ((j / C::NPB) - 1) & 1);
           sm100::tc_fence_after();
         }
+        const uint32_t tP = p_buf(j);
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {
-          sm100::mma_pair_ts<V == kTF32>(tmem_P, ahi + 8 * ks, bhi + kB * ks, b_hi_w, idesc,
+          sm100::mma_pair_ts_el<V == kTF32>(tP, ahi + 8 * ks, bhi + kB * ks, b_hi_w, idesc,
                                          !(first_in_interval && ks == 0));
         }
-        sm100::mma_commit_pair_mc(&op_empty[o], 0x3);
-        if ((kb % de) == de - 1 || kb == nop - 1) sm100::mma_commit_pair_mc(p_full, 0x3);
+        sm100::mma_commit_pair_mc_el(&op_empty[o], 0x3);
+        if ((kb % de) == de - 1 || kb == nop - 1) sm100::mma_commit_pair_mc_el(&p_full[b], 0x3);
       }
     }
   } else if (warp < C::DRAIN_WARP0) {
@@ -341,12 +356,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
 #pragma unroll
     for (int j = 0; j < NC; ++j) acc[j] = 0.0f;
     for (int it = 0; it < nintervals; ++it) {
-      sm100::mbar_wait(p_full, it & 1);
+      const int b = it % C::NPB;
+      sm100::mbar_wait(&p_full[b], (it / C::NPB) & 1);
       sm100::tc_fence_after();
+      const uint32_t tP = p_buf(it);
 #pragma unroll
       for (int c = 0; c < NC / 16; ++c) {
         uint32_t r[16];
-        sm100::tmem_ld_32x32b_x16(tmem_P + lane_off + h * NC + c * 16, r);
+        sm100::tmem_ld_32x32b_x16(tP + lane_off + h * NC + c * 16, r);
         sm100::tmem_ld_wait();
 #pragma unroll
         for (int j = 0; j < 16; ++j)  // schemes.py:300-304: c = RN32(c + partial)
@@ -354,7 +371,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
       }
       sm100::tc_fence_before();
       __syncwarp();
-      if (lane == 0) sm100::mbar_arrive_remote(p_empty_leader);
+      if (lane == 0) sm100::mbar_arrive_remote(p_empty_leader + b * 8);
     }
     bool nonfinite = false;
     // the split warps' staging reads precede the epilogue's staging writes

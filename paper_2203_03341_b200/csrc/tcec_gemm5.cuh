@@ -191,7 +191,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
                                n_cta + 32 * b, st * C::BK_STG);
         }
       }
-    } else if (warp == 1 && lane == 0 && rank == 0) {
+    } else if (warp == 1 && rank == 0) {  // the whole warp runs the issue loop; one elected lane issues
       // ===================== MMA issuer (leader CTA) =====================
       constexpr uint32_t idesc = sm100::umma_idesc_bmn(VC::AB_FORMAT, 2 * C::BM, C::BN);
       constexpr uint32_t a_hi_w = (1024u >> 4) | (1u << 14) | (2u << 29);
@@ -220,13 +220,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<V>::NUM_THRE
           c3_stage(
               kb * 4, 4 * nop_u, de, pos, git, p_empty, p_full, &op_empty[o],
               [&](int ks) {  // schemes.py:294-298: dA*B_hi, then A_hi*dB
-                sm100::mma_pair_split<V == kTF32>(tmem_dC, alo + 2 * ks, a_hi_w, bhi + kB * ks,
+                sm100::mma_pair_split_el<V == kTF32>(tmem_dC, alo + 2 * ks, a_hi_w, bhi + kB * ks,
                                                   b_hi_w, idesc, (kb | ks) != 0);
-                sm100::mma_pair_split<V == kTF32>(tmem_dC, ahi + 2 * ks, a_hi_w, blo + kB * ks,
+                sm100::mma_pair_split_el<V == kTF32>(tmem_dC, ahi + 2 * ks, a_hi_w, blo + kB * ks,
                                                   b_hi_w, idesc, 1u);
               },
               [&](int ks, uint32_t acc) {
-                sm100::mma_pair_split<V == kTF32>(tmem_P, ahi + 2 * ks, a_hi_w, bhi + kB * ks,
+                sm100::mma_pair_split_el<V == kTF32>(tmem_P, ahi + 2 * ks, a_hi_w, bhi + kB * ks,
                                                   b_hi_w, idesc, acc);
               });
         }

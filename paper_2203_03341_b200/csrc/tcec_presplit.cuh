@@ -303,7 +303,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PsCfg<V, S>::NUM_THR
           }
         }
       }
-    } else if (warp == 1 && lane == 0 && rank == 0) {
+    } else if (warp == 1 && rank == 0) {  // the whole warp runs the issue loop; one elected lane issues
       // ===================== MMA issuer (leader CTA) =====================
       constexpr uint32_t idesc = sm100::umma_idesc(VC::AB_FORMAT, 2 * C::BM, C::BN);
       constexpr uint32_t hi_w = (1024u >> 4) | (1u << 14) | (2u << 29);  // SBO 1024, v1, SW128
@@ -328,7 +328,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PsCfg<V, S>::NUM_THR
           if constexpr (S == kSchPlain) {
 #pragma unroll
             for (int ks = 0; ks < 4; ++ks)
-              sm100::mma_pair_split<V == kTF32>(tmem_P, ahi + 2 * ks, hi_w, bhi + 2 * ks, hi_w, idesc,
+              sm100::mma_pair_split_el<V == kTF32>(tmem_P, ahi + 2 * ks, hi_w, bhi + 2 * ks, hi_w, idesc,
                                                 (kb | ks) != 0);
           } else if constexpr (S == kSchIn4RN) {
             // per MMA k-step, the four terms in the reference's order, each into
@@ -344,12 +344,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PsCfg<V, S>::NUM_THR
                   sm100::mbar_wait_cluster(&p_empty[t], (git - 1) & 1);
                   sm100::tc_fence_after();
                 }
-                sm100::mma_pair_split<V == kTF32>(tmem_P + t * C::BN, (t < 2 ? alo : ahi) + 2 * ks,
+                sm100::mma_pair_split_el<V == kTF32>(tmem_P + t * C::BN, (t < 2 ? alo : ahi) + 2 * ks,
                                                   hi_w, ((t & 1) ? bhi : blo) + 2 * ks, hi_w, idesc,
                                                   !first);
               }
               if ((kk % de) == de - 1 || (kb == nop - 1 && ks == 3)) {
-                sm100::mma_commit_pair_mc(p_full, 0x3);
+                sm100::mma_commit_pair_mc_el(p_full, 0x3);
                 ++git;
               }
             }
@@ -357,33 +357,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PsCfg<V, S>::NUM_THR
             // the reference's four-call order per block: dA*dB, dA*B, A*dB, A*B
 #pragma unroll
             for (int ks = 0; ks < 4; ++ks) {
-              sm100::mma_pair_split<V == kTF32>(tmem_P, alo + 2 * ks, hi_w, blo + 2 * ks, hi_w, idesc,
+              sm100::mma_pair_split_el<V == kTF32>(tmem_P, alo + 2 * ks, hi_w, blo + 2 * ks, hi_w, idesc,
                                                 (kb | ks) != 0);
-              sm100::mma_pair_split<V == kTF32>(tmem_P, alo + 2 * ks, hi_w, bhi + 2 * ks, hi_w, idesc, 1u);
-              sm100::mma_pair_split<V == kTF32>(tmem_P, ahi + 2 * ks, hi_w, blo + 2 * ks, hi_w, idesc, 1u);
-              sm100::mma_pair_split<V == kTF32>(tmem_P, ahi + 2 * ks, hi_w, bhi + 2 * ks, hi_w, idesc, 1u);
+              sm100::mma_pair_split_el<V == kTF32>(tmem_P, alo + 2 * ks, hi_w, bhi + 2 * ks, hi_w, idesc, 1u);
+              sm100::mma_pair_split_el<V == kTF32>(tmem_P, ahi + 2 * ks, hi_w, blo + 2 * ks, hi_w, idesc, 1u);
+              sm100::mma_pair_split_el<V == kTF32>(tmem_P, ahi + 2 * ks, hi_w, bhi + 2 * ks, hi_w, idesc, 1u);
             }
           } else {
             c3_stage(
                 kb * 4, 4 * nop, de, pos, git, p_empty, p_full, &op_empty[o],
                 [&](int ks) {  // reference order per k-step: dA*B then A*dB (schemes.py:294-298)
-                  sm100::mma_pair_split<V == kTF32>(tmem_dC, alo + 2 * ks, hi_w, bhi + 2 * ks, hi_w,
+                  sm100::mma_pair_split_el<V == kTF32>(tmem_dC, alo + 2 * ks, hi_w, bhi + 2 * ks, hi_w,
                                                     idesc, (kb | ks) != 0);
-                  sm100::mma_pair_split<V == kTF32>(tmem_dC, ahi + 2 * ks, hi_w, blo + 2 * ks, hi_w,
+                  sm100::mma_pair_split_el<V == kTF32>(tmem_dC, ahi + 2 * ks, hi_w, blo + 2 * ks, hi_w,
                                                     idesc, 1u);
                   if constexpr (S == kSchC3DD)  // schemes.py:308-313: the dA*dB chain
-                    sm100::mma_pair_split<V == kTF32>(tmem_ddC, alo + 2 * ks, hi_w, blo + 2 * ks,
+                    sm100::mma_pair_split_el<V == kTF32>(tmem_ddC, alo + 2 * ks, hi_w, blo + 2 * ks,
                                                       hi_w, idesc, (kb | ks) != 0);
                 },
                 [&](int ks, uint32_t acc) {
-                  sm100::mma_pair_split<V == kTF32>(tmem_P, ahi + 2 * ks, hi_w, bhi + 2 * ks, hi_w,
+                  sm100::mma_pair_split_el<V == kTF32>(tmem_P, ahi + 2 * ks, hi_w, bhi + 2 * ks, hi_w,
                                                     idesc, acc);
                 });
           }
           if constexpr (!C::kDrain)  // (c3_stage commits op_empty itself)
-            sm100::mma_commit_pair_mc(&op_empty[o], 0x3);
+            sm100::mma_commit_pair_mc_el(&op_empty[o], 0x3);
           if ((S == kSchPlain || S == kSchIn4) && kb == nop - 1) {
-            sm100::mma_commit_pair_mc(p_full, 0x3);
+            sm100::mma_commit_pair_mc_el(p_full, 0x3);
             ++git;
           }
         }

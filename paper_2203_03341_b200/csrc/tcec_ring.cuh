@@ -404,7 +404,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
           if (spin > (1u << 26)) __trap();
         }
       }
-    } else if (warp == 1 && lane == 0 && rank == 0) {
+    } else if (warp == 1 && rank == 0) {  // the whole warp runs the issue loop; one elected lane issues
       // ===================== MMA issuer (leader CTA) =====================
       constexpr uint32_t idesc = sm100::umma_idesc(VC::AB_FORMAT, 2 * C::BM, C::BN);
       constexpr uint32_t hi_w = (1024u >> 4) | (1u << 14) | (2u << 29);  // SBO 1024, v1, SW128
@@ -427,13 +427,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(640, 1)
           c3_stage(
               kb * 4, 4 * nop, de, pos, git, p_empty, p_full, &op_empty[o],
               [&](int ks) {  // reference order per k-step: dA*B_hi, then A_hi*dB (schemes.py:294-298)
-                sm100::mma_pair_split<V == kTF32>(tmem_dC, alo + 2 * ks, hi_w, bhi + 2 * ks, hi_w,
+                sm100::mma_pair_split_el<V == kTF32>(tmem_dC, alo + 2 * ks, hi_w, bhi + 2 * ks, hi_w,
                                                   idesc, (kb | ks) != 0);
-                sm100::mma_pair_split<V == kTF32>(tmem_dC, ahi + 2 * ks, hi_w, blo + 2 * ks, hi_w,
+                sm100::mma_pair_split_el<V == kTF32>(tmem_dC, ahi + 2 * ks, hi_w, blo + 2 * ks, hi_w,
                                                   idesc, 1u);
               },
               [&](int ks, uint32_t acc) {
-                sm100::mma_pair_split<V == kTF32>(tmem_P, ahi + 2 * ks, hi_w, bhi + 2 * ks, hi_w,
+                sm100::mma_pair_split_el<V == kTF32>(tmem_P, ahi + 2 * ks, hi_w, bhi + 2 * ks, hi_w,
                                                   idesc, acc);
               });
         }
