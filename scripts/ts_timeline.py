@@ -1,3 +1,5 @@
+# Needs a measurement build of the 256 x 64 kernel with globaltimer stamps per
+# stage (profiles/r02/elect/README.md); prints the per-stage timeline of one CTA.
 import os, sys, torch
 sys.path.insert(0, os.getcwd())
 import paper_2203_03341_b200 as T
