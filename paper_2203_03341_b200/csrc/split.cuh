@@ -31,6 +31,21 @@ constexpr uint32_t kFlagNonfiniteInput = 4u;
 // cvt.{rn,rz}.f16x2.f32: IEEE conversion with gradual underflow; RN overflows
 // to inf (formats.py:140); RZ saturates to 65504 (formats.py:137-138), which
 // needs .satfinite (plain cvt.rz returns inf for inputs near FLT_MAX).
+// 0xFFFF in each half of a packed FP16 pair that is not +-inf (NaN included),
+// 0 where it is: abs.f16x2 folds into the HSET2 compare.
+__device__ __forceinline__ uint32_t f16x2_finite_mask(uint32_t h) {
+  uint32_t m;
+  asm("{\n"
+      ".reg .b32 a, b;\n"
+      "abs.f16x2 a, %1;\n"
+      "mov.b32 b, 0x7c007c00;\n"
+      "set.neu.u32.f16x2 %0, a, b;\n"
+      "}"
+      : "=r"(m)
+      : "r"(h));
+  return m;
+}
+
 template <int R>
 __device__ __forceinline__ uint32_t cvt_f16x2(float lo_elem, float hi_elem) {
   uint32_t d;

@@ -131,8 +131,9 @@ __device__ __forceinline__ void c3_stage(int j0, int nks, int de, int& pos, uint
 // (FP16: 8 values -> 4 packed half2 words each; TF32: 4 values -> 4 words,
 // the rounded FP32 bit patterns), splitting.py:114-122:
 //   hi = round(x), lo = round((x - hi) 2^s), lo = 0 where hi overflowed
-// (a select per element: measured cheaper than guarding a rare fix-up with a
-// max over the inputs, which costs the 56-register split warps more).
+// (FP16: a packed mask per half2; TF32: a select per element -- both measured
+// cheaper than guarding a rare fix-up with a max over the inputs, which costs
+// the 56-register split warps more).
 template <int V, int R>
 __device__ __forceinline__ void split_chunk(const float* x, float scale, uint32_t (&hw)[4],
                                             uint32_t (&lw)[4]) {
@@ -144,11 +145,11 @@ __device__ __forceinline__ void split_chunk(const float* x, float scale, uint32_
       float h0, h1, r0, r1;
       unpack_f16x2(hw[j], h0, h1);
       sm100::residual_x2(x[2 * j], x[2 * j + 1], h0, h1, scale, r0, r1);
-      if constexpr (kFix) {
-        r0 = isinf(h0) ? 0.0f : r0;
-        r1 = isinf(h1) ? 0.0f : r1;
-      }
       lw[j] = cvt_f16x2<R>(r0, r1);
+      // lo = 0 where hi = +-inf: one packed compare on |hi| (HSET2) and a mask,
+      // instead of a compare and select per element (the residual there is
+      // -+inf, so only those halves change; NaN keeps its NaN lo)
+      if constexpr (kFix) lw[j] &= f16x2_finite_mask(hw[j]);
     }
   } else {
 #pragma unroll
