@@ -77,8 +77,14 @@ def test_argument_validation_without_gpu(lib):
     # the narrow tiles drain whole operand stages; the single-CTA kernel is block_n 128 only
     o = N.make_opts(drain_k=16, block_n=192)
     assert f(0, 4, 4, 4, None, 4, None, 4, None, 4, ctypes.byref(o), None, None) == N.ERR_UNSUPPORTED
+    o = N.make_opts(drain_k=16, block_n=64)
+    assert f(0, 4, 4, 4, None, 4, None, 4, None, 4, ctypes.byref(o), None, None) == N.ERR_UNSUPPORTED
     o = N.make_opts(kernel_variant=1)
     assert f(0, 4, 4, 4, None, 4, None, 4, None, 4, ctypes.byref(o), None, None) == N.ERR_UNSUPPORTED
+    # tile widths are 64 / 128 / 192 / 256 (0 = automatic)
+    for bn in (32, 96, 320):
+        o = N.make_opts(block_n=bn)
+        assert f(0, 4, 4, 4, None, 4, None, 4, None, 4, ctypes.byref(o), None, None) == N.ERR_UNSUPPORTED
     o = N.make_opts(scale_log2=11)
     assert f(1, 4, 4, 4, None, 4, None, 4, None, 4, ctypes.byref(o), None, None) == N.ERR_UNSUPPORTED
     # corrected4_rn blocks are whole MMA k-steps; split_k in 0..64; kernel variants 0..4
