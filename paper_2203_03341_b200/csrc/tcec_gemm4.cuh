@@ -32,7 +32,6 @@ struct TsCfg {
   static constexpr int BN = BN_;           // pair N = MMA N (192, or 128 with a deeper ring)
   static constexpr int BN_CTA = BN / 2;    // B columns staged / split per CTA
   static constexpr int BK_STG = 32;        // FP32 k per staging slice
-  static constexpr int NSTG = 4;
   static constexpr int NOP = NOP_;         // operand ring (B in smem, A in TMEM)
   static constexpr int STG_A_BYTES = BM * BK_STG * 4;      // 16 KB, SW128 rows of 32 k
   static constexpr int STG_B_BOX = BK_STG * 32 * 4;        // 4 KB box: 32 k x 32 n, SW128
@@ -42,6 +41,12 @@ struct TsCfg {
   static constexpr int ESIZE = V == kFP16 ? 2 : 4;
   static constexpr int OP_B_BYTES = BN_CTA * VarCfg<V>::BK_OP * ESIZE;  // 12 KB
   static constexpr int OP_BYTES = 2 * OP_B_BYTES;                      // B_hi | B_lo
+  // FP32 staging ring: as deep as shared memory allows, up to 8 slices.  These
+  // tiles' MMAs are short, so the TMA latency (~0.9 us under load, measured by
+  // a per-stage timeline of the 256 x 64 kernel) must be covered by slices in
+  // flight rather than by MMA time.
+  static constexpr int NSTG_FIT = (225 * 1024 - NOP * OP_BYTES) / STG_BYTES;
+  static constexpr int NSTG = NSTG_FIT < 8 ? NSTG_FIT : 8;
   // MN-major B atoms: 32 n per row (FP16 SWIZZLE_64B: 64-byte rows, 8 k rows;
   // TF32 SWIZZLE_128B_BASE32B: 128-byte rows, 4 k rows); atoms along n (LBO),
   // then k-groups (SBO).
@@ -119,44 +124,52 @@ __device__ __forceinline__ void ts_split_slice(uint32_t stg, uint32_t op, uint32
       sm100::tmem_st_32x32b_x16(ta + lanes + 32 + col, lw);
     }
   }
-  // ---- B -> shared memory (MN-major)
-  if (t < 32 * 2 * C::NUM_B_BOXES) {
-    const int row = t & 31, qn = t >> 5;
-    const uint32_t box = stg + C::STG_A_BYTES + (qn >> 1) * C::STG_B_BOX;
-    const int h = V == kTF32 ? (t >> 2) & 1 : 0;  // TF32 chunk order (conflict-free STS)
-    float x[16];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float4 v = sm100::lds128(box + sw128(row, (qn & 1) * 4 + (i ^ h)));
-      x[4 * i] = v.x; x[4 * i + 1] = v.y; x[4 * i + 2] = v.z; x[4 * i + 3] = v.w;
-    }
-    if constexpr (kFlags) {
-#pragma unroll
-      for (int i = 0; i < 16; ++i) fa.add(x[i]);
-    }
-    uint32_t hw[16], lw[16];
-    split16<V, R>(x, scale, hw, lw);
-    const int kop = sub * 32 + row;  // k within the operand stage
-    const int grp = kop / C::B_ROWS, rr = kop % C::B_ROWS;
-    const uint32_t base = grp * C::B_SBO + (qn >> 1) * C::B_LBO + rr * C::B_ROW_BYTES;
+  // ---- B -> shared memory (MN-major), spread over all 256 split threads: per
+  // 32-column box, each thread splits 4 consecutive n of one k row (so the
+  // B work no longer doubles the split time of the first 2 x NUM_B_BOXES
+  // warps -- the step that bounded the narrow tiles).  Lane layout per warp:
+  // 16 k rows x 8 n, chosen so that the 16-byte LDS phases and the STS phases
+  // (FP16: 64-bit stores into SW64 rows; TF32: 128-bit stores into
+  // SW128_BASE32B rows) hit distinct banks.
+  {
+    const int w = t >> 5, l = t & 31;
     const uint32_t hi_base = op, lo_base = op + C::OP_B_BYTES;
-    if constexpr (V == kFP16) {
-      // SW64 (Swizzle<2,4,3>): 16-byte chunk ^ ((row >> 1) & 3); 16 n = chunks 2 (qn & 1) + {0, 1}
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int c16 = (qn & 1) * 2 + q;
-        const uint32_t off = base + (((c16 ^ (rr >> 1)) & 3) << 4);
-        sm100::sts128(hi_base + off, hw[4 * q], hw[4 * q + 1], hw[4 * q + 2], hw[4 * q + 3]);
-        sm100::sts128(lo_base + off, lw[4 * q], lw[4 * q + 1], lw[4 * q + 2], lw[4 * q + 3]);
+    for (int bx = 0; bx < C::NUM_B_BOXES; ++bx) {
+      int row, c16;  // k within the slice; 16-byte (4 n) chunk within the box
+      if constexpr (V == kFP16) {
+        row = (w & 1) * 16 + (l >> 4) * 8 + (l & 7);
+        c16 = (w >> 1) * 2 + ((l >> 3) & 1);
+      } else {
+        row = (w & 1) * 16 + (l >> 3) * 4 + (l & 3);
+        c16 = (w >> 1) * 2 + ((l >> 2) & 1);
       }
-    } else {
-      // SW128_BASE32B (Swizzle<2,5,2>): 32-byte chunk ^ (row & 3); 16 n = 16-byte chunks 4 (qn & 1) + q
+      const uint32_t box = stg + C::STG_A_BYTES + bx * C::STG_B_BOX;
+      const float4 v = sm100::lds128(box + sw128(row, c16));
+      float x[4] = {v.x, v.y, v.z, v.w};
+      if constexpr (kFlags) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int c16 = (qn & 1) * 4 + (q ^ h);
+        for (int i = 0; i < 4; ++i) fa.add(x[i]);
+      }
+      const int kop = sub * 32 + row;  // k within the operand stage
+      const int grp = kop / C::B_ROWS, rr = kop % C::B_ROWS;
+      const uint32_t base = grp * C::B_SBO + bx * C::B_LBO + rr * C::B_ROW_BYTES;
+      if constexpr (V == kFP16) {
+        uint32_t hw[2], lw[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) split_pair16<R>(x[2 * j], x[2 * j + 1], scale, hw[j], lw[j]);
+        // SW64 (Swizzle<2,4,3>): 16-byte chunk (8 n) ^ ((row >> 1) & 3); 4 n = half a chunk
+        const int c8 = c16 >> 1;
+        const uint32_t off = base + (((c8 ^ (rr >> 1)) & 3) << 4) + ((c16 & 1) << 3);
+        sm100::sts64(hi_base + off, hw[0], hw[1]);
+        sm100::sts64(lo_base + off, lw[0], lw[1]);
+      } else {
+        uint32_t hw[4], lw[4];
+        split_chunk<V, R>(x, scale, hw, lw);
+        // SW128_BASE32B (Swizzle<2,5,2>): 32-byte chunk ^ (row & 3)
         const uint32_t off = base + ((((c16 >> 1) ^ rr) & 3) << 5) + ((c16 & 1) << 4);
-        sm100::sts128(hi_base + off, hw[4 * q], hw[4 * q + 1], hw[4 * q + 2], hw[4 * q + 3]);
-        sm100::sts128(lo_base + off, lw[4 * q], lw[4 * q + 1], lw[4 * q + 2], lw[4 * q + 3]);
+        sm100::sts128(hi_base + off, hw[0], hw[1], hw[2], hw[3]);
+        sm100::sts128(lo_base + off, lw[0], lw[1], lw[2], lw[3]);
       }
     }
   }
