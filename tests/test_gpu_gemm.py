@@ -1134,3 +1134,34 @@ def test_out_argument_is_validated():
     out = torch.full((64, 48), float("nan"), device="cuda")
     T.gemm_device(a, b, "corrected3_tf32", out=out)
     assert torch.equal(out, T.gemm_device(a, b, "corrected3_tf32"))
+
+
+@pytest.mark.parametrize("sname", ["corrected3_halfhalf", "corrected3_tf32"])
+@pytest.mark.parametrize("kv", [2, 3])
+def test_persistent_runflags_cover_every_element(sname, kv):
+    """RunFlags from the persistent kernels (kernel_variant 2 / 3: the
+    designated CTAs of tile row 0 and tile column 0 fold the inputs) equal the
+    per-tile kernel's for a single special input anywhere -- first / last k
+    stage, ragged row / column, inside A or B; a NaN is always flagged."""
+    import torch
+
+    T = _T()
+    m, n, k = 1100, 900, 3000
+    g = torch.Generator(device="cuda")
+    g.manual_seed(7)
+    A0 = torch.rand((m, k), generator=g, device="cuda") * 2 - 1
+    B0 = torch.rand((k, n), generator=g, device="cuda") * 2 - 1
+    positions = [("A", 0, 0), ("A", m - 1, k - 1), ("A", 517, 1999), ("A", 1099, 64),
+                 ("B", 0, 0), ("B", k - 1, n - 1), ("B", 1234, 777), ("B", 31, 899)]
+    specials = [float("nan"), 1e-30, 7e4 if sname == "corrected3_halfhalf" else 3.4e38]
+    for which, i, j in positions:
+        for val in specials:
+            A, B = A0.clone(), B0.clone()
+            (A if which == "A" else B)[i, j] = val
+            f_ref = torch.zeros(1, dtype=torch.int32, device="cuda")
+            f_per = torch.zeros(1, dtype=torch.int32, device="cuda")
+            T.gemm_device(A, B, sname, flags=f_ref, kernel_variant=4)
+            T.gemm_device(A, B, sname, flags=f_per, kernel_variant=kv)
+            if val != val:
+                assert int(f_ref.item()) != 0, (which, i, j, val)
+            assert int(f_per.item()) == int(f_ref.item()), (which, i, j, val, kv)
