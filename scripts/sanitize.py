@@ -17,7 +17,7 @@ runs = []
 for sname in ("corrected3_halfhalf", "corrected3_tf32"):
     ref = T.gemm_device(A, B, sname, kernel_variant=4)
     for kw in ({}, {"kernel_variant": 2}, {"kernel_variant": 3},
-               {"block_n": 192}, {"block_n": 128}, {"block_n": 128, "kernel_variant": 1},
+               {"block_n": 192}, {"block_n": 128}, {"block_n": 64}, {"block_n": 128, "kernel_variant": 1},
                {"split_mode": 2}, {"drain_k": 16 if "half" in sname else 8},
                {"split_k": 2}):
         c = T.gemm_device(A, B, sname, **kw)
