@@ -561,7 +561,7 @@ def main():
                        "path": "paper_2203_03341_b200.gemm(numpy pinned) -> tcec_sgemm_host"}
         del run
 
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:  # the CPU arm: N = 1 only
         line["cpu_baseline"] = cpu_oracle_sample(args.variant, n, args.cpu_sample_seconds,
                                                  os.cpu_count() or 1, spec=spec)
         line["cpu_baseline"].pop("seconds", None)
