@@ -18,6 +18,8 @@
 #include <cstring>
 #include <cuda_fp16.h>
 
+#include "sm100.cuh"
+
 namespace tcec {
 
 enum Variant : int { kFP16 = 0, kTF32 = 1 };
@@ -64,19 +66,27 @@ __device__ __forceinline__ void unpack_f16x2(uint32_t p, float& a, float& b) {
 }
 
 // Two consecutive elements -> packed (hi, lo) half2 words, element 0 in the
-// low half (lower address once stored).
+// low half (lower address once stored) -- the split warps' arithmetic: the
+// residual (x - hi) 2^s as one fma.rn.f32x2 (both products exact, one rounding
+// of a representable value), and splitting.py:119-121 (lo = 0 where hi
+// overflowed) as one packed compare on |hi| and a mask: the residual there is
+// -+inf, so only those halves change; a NaN input keeps its NaN lo.
+template <int R>
+__device__ __forceinline__ void split_pair16(float x0, float x1, float scale, uint32_t& hw,
+                                             uint32_t& lw) {
+  constexpr bool kFix = R != kRZ;  // RZ saturates: hi never overflows
+  hw = cvt_f16x2<R>(x0, x1);
+  float h0, h1, r0, r1;
+  unpack_f16x2(hw, h0, h1);
+  sm100::residual_x2(x0, x1, h0, h1, scale, r0, r1);
+  lw = cvt_f16x2<R>(r0, r1);
+  if constexpr (kFix) lw &= f16x2_finite_mask(hw);
+}
+
 template <int R>
 __device__ __forceinline__ void split_f16_pair(float x0, float x1, float scale, uint32_t& hi,
                                                uint32_t& lo) {
-  hi = cvt_f16x2<R>(x0, x1);
-  float h0, h1;
-  unpack_f16x2(hi, h0, h1);
-  // splitting.py:119-121: where hi overflowed the residual is taken as 0.
-  h0 = isinf(h0) ? x0 : h0;
-  h1 = isinf(h1) ? x1 : h1;
-  const float r0 = __fmul_rn(__fsub_rn(x0, h0), scale);
-  const float r1 = __fmul_rn(__fsub_rn(x1, h1), scale);
-  lo = cvt_f16x2<R>(r0, r1);
+  split_pair16<R>(x0, x1, scale, hi, lo);
 }
 
 // ------------------------------------------------------------------ TF32 --
@@ -109,13 +119,19 @@ __device__ __forceinline__ uint32_t tf32_carry_bits(uint32_t u) {
   }
 }
 
+// One element, the split warps' arithmetic (split_chunk in tcec_gemm2.cuh runs
+// it on pairs with sub.rn.f32x2): lo's rounding carry on the exact residual,
+// 0 where x - hi is infinite, i.e. where hi overflowed (splitting.py:119-121);
+// the low 13 bits are cleared here (the tensor core ignores them in the GEMM).
+// TF32 has no residual scale (tf32tf32: s = 0).
 template <int R>
 __device__ __forceinline__ void split_tf32(float x, float scale, float& hi, float& lo) {
-  const float h = __uint_as_float(tf32_round_bits<R>(__float_as_uint(x)));
-  const float he = isinf(h) ? x : h;
-  const float r = __fmul_rn(__fsub_rn(x, he), scale);
-  hi = h;
-  lo = __uint_as_float(tf32_round_bits<R>(__float_as_uint(r)));
+  (void)scale;
+  const uint32_t hb = tf32_round_bits<R>(__float_as_uint(x));
+  const float r = __fsub_rn(x, __uint_as_float(hb));
+  const uint32_t lb = (R != kRZ && isinf(r)) ? 0u : tf32_carry_bits<R>(__float_as_uint(r));
+  hi = __uint_as_float(hb);
+  lo = __uint_as_float(lb & 0xFFFFE000u);
 }
 
 // ----------------------------------------------------------------- flags --

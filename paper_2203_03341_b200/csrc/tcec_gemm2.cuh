@@ -134,22 +134,6 @@ __device__ __forceinline__ void c3_stage(int j0, int nks, int de, int& pos, uint
 // (FP16: a packed mask per half2; TF32: a select per element -- both measured
 // cheaper than guarding a rare fix-up with a max over the inputs, which costs
 // the 56-register split warps more).
-// One FP16 pair: packed hi and lo words.  lo = 0 where hi = +-inf: one packed
-// compare on |hi| (HSET2) and a mask, instead of a compare and select per
-// element (the residual there is -+inf, so only those halves change; NaN keeps
-// its NaN lo).
-template <int R>
-__device__ __forceinline__ void split_pair16(float x0, float x1, float scale, uint32_t& hw,
-                                             uint32_t& lw) {
-  constexpr bool kFix = R != kRZ;  // RZ saturates: hi never overflows
-  hw = cvt_f16x2<R>(x0, x1);
-  float h0, h1, r0, r1;
-  unpack_f16x2(hw, h0, h1);
-  sm100::residual_x2(x0, x1, h0, h1, scale, r0, r1);
-  lw = cvt_f16x2<R>(r0, r1);
-  if constexpr (kFix) lw &= f16x2_finite_mask(hw);
-}
-
 template <int V, int R>
 __device__ __forceinline__ void split_chunk(const float* x, float scale, uint32_t (&hw)[4],
                                             uint32_t (&lw)[4]) {
