@@ -503,38 +503,6 @@ __device__ __forceinline__ void tmem_st_wait() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
-// mma_pair_split with an A-operand collector hint (kC: 0 none, 1 fill = keep A
-// for the next MMA, 2 use = reuse and keep, 3 lastuse = reuse then release).
-template <bool kTF32, int kC>
-__device__ __forceinline__ void mma_pair_col(uint32_t d_tmem, uint32_t a_lo, uint32_t a_hi,
-                                             uint32_t b_lo, uint32_t b_hi, uint32_t idesc,
-                                             uint32_t accumulate) {
-#define TCEC_MMA_COL(KIND, COL)                                                   \
-  asm volatile(                                                                   \
-      "{\n"                                                                       \
-      ".reg .pred p;\n"                                                           \
-      ".reg .b64 ad, bd;\n"                                                       \
-      "mov.b64 ad, {%1, %2};\n"                                                   \
-      "mov.b64 bd, {%3, %4};\n"                                                   \
-      "setp.ne.b32 p, %6, 0;\n"                                                   \
-      "tcgen05.mma.cta_group::2.kind::" KIND COL " [%0], ad, bd, %5, p;\n"         \
-      "}\n" ::"r"(d_tmem),                                                        \
-      "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(accumulate)     \
-      : "memory")
-  if constexpr (kTF32) {
-    if constexpr (kC == 0) TCEC_MMA_COL("tf32", "");
-    else if constexpr (kC == 1) TCEC_MMA_COL("tf32", ".collector::a::fill");
-    else if constexpr (kC == 2) TCEC_MMA_COL("tf32", ".collector::a::use");
-    else TCEC_MMA_COL("tf32", ".collector::a::lastuse");
-  } else {
-    if constexpr (kC == 0) TCEC_MMA_COL("f16", "");
-    else if constexpr (kC == 1) TCEC_MMA_COL("f16", ".collector::a::fill");
-    else if constexpr (kC == 2) TCEC_MMA_COL("f16", ".collector::a::use");
-    else TCEC_MMA_COL("f16", ".collector::a::lastuse");
-  }
-#undef TCEC_MMA_COL
-}
-
 // Hide a value from the optimiser (stops it hoisting per-stage descriptor
 // math for every ring slot into registers).
 __device__ __forceinline__ uint32_t opaque(uint32_t x) {
