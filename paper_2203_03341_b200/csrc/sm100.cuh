@@ -17,12 +17,6 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-__device__ __forceinline__ uint32_t lane_id() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%laneid;" : "=r"(r));
-  return r;
-}
-
 // ------------------------------------------------------- shared-memory I/O --
 // Explicit shared-window accesses on 32-bit addresses (never generic LD/ST).
 __device__ __forceinline__ float4 lds128(uint32_t addr) {
@@ -106,14 +100,6 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* m, uin
       : "memory");
 }
 
-// Warm L2 with a tile the TMA will load later (no shared memory, no barrier).
-__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* m, int32_t c0, int32_t c1) {
-  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
-                   reinterpret_cast<uint64_t>(m)),
-               "r"(c0), "r"(c1)
-               : "memory");
-}
-
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, const void* src, int32_t c0,
                                              int32_t c1) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
@@ -123,9 +109,6 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, const void* s
 }
 __device__ __forceinline__ void tma_store_commit() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-__device__ __forceinline__ void tma_store_wait_read0() {
-  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 __device__ __forceinline__ void tma_store_wait0() {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -252,32 +235,12 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
   return r;
 }
 
-// Arrive on an mbarrier in another CTA of the cluster (release at cluster scope).
-__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
-               : "memory");
-}
-
 // Named barrier over `kThreads` threads (warp multiples) of this CTA; the
 // non-.aligned form, so lanes that left a lane-0 branch need not reconverge.
 template <uint32_t kId, uint32_t kThreads>
 __device__ __forceinline__ void named_barrier_sync() {
   __syncwarp();
   asm volatile("barrier.sync %0, %1;" ::"n"(kId), "n"(kThreads) : "memory");
-}
-
-// 16-byte store into another CTA's shared memory (shared::cluster address).
-__device__ __forceinline__ void sts128_cluster(uint32_t cluster_addr, uint32_t a, uint32_t b,
-                                               uint32_t c, uint32_t d) {
-  asm volatile("st.shared::cluster.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(cluster_addr), "r"(a),
-               "r"(b), "r"(c), "r"(d)
-               : "memory");
-}
-
-// Order this thread's generic-proxy shared-memory writes (local and in peer
-// CTAs) before later async-proxy (tensor core) reads of them.
-__device__ __forceinline__ void fence_proxy_async_cluster() {
-  asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");
 }
 
 // Arrive on an mbarrier in another CTA of the cluster with the default
@@ -330,97 +293,14 @@ __device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr) {
                : "memory");
 }
 
-// CTA-pair MMA (M = 256 across the pair), issued by the leader CTA only.
-template <bool kTF32>
-__device__ __forceinline__ void mma_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
-                                         uint32_t idesc, uint32_t accumulate) {
-  if constexpr (kTF32) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "setp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
-        "}\n" ::"r"(d_tmem),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-        : "memory");
-  } else {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "setp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
-        "}\n" ::"r"(d_tmem),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-        : "memory");
-  }
-}
-
-// Same, with each descriptor given as (low, high) 32-bit halves so the issuer
-// keeps only 32-bit state in registers.
-template <bool kTF32>
-__device__ __forceinline__ void mma_pair_split(uint32_t d_tmem, uint32_t a_lo, uint32_t a_hi,
-                                               uint32_t b_lo, uint32_t b_hi, uint32_t idesc,
-                                               uint32_t accumulate) {
-  if constexpr (kTF32) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        ".reg .b64 ad, bd;\n"
-        "mov.b64 ad, {%1, %2};\n"
-        "mov.b64 bd, {%3, %4};\n"
-        "setp.ne.b32 p, %6, 0;\n"
-        "tcgen05.mma.cta_group::2.kind::tf32 [%0], ad, bd, %5, p;\n"
-        "}\n" ::"r"(d_tmem),
-        "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(accumulate)
-        : "memory");
-  } else {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        ".reg .b64 ad, bd;\n"
-        "mov.b64 ad, {%1, %2};\n"
-        "mov.b64 bd, {%3, %4};\n"
-        "setp.ne.b32 p, %6, 0;\n"
-        "tcgen05.mma.cta_group::2.kind::f16 [%0], ad, bd, %5, p;\n"
-        "}\n" ::"r"(d_tmem),
-        "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(accumulate)
-        : "memory");
-  }
-}
-
-// CTA-pair MMA with the A operand in tensor memory (each CTA's TMEM holds its
-// 128 rows: lane = row, column = 32-bit word of K) and B from shared memory.
-template <bool kTF32>
-__device__ __forceinline__ void mma_pair_ts(uint32_t d_tmem, uint32_t a_tmem, uint32_t b_lo,
-                                            uint32_t b_hi, uint32_t idesc, uint32_t accumulate) {
-  if constexpr (kTF32) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        ".reg .b64 bd;\n"
-        "mov.b64 bd, {%2, %3};\n"
-        "setp.ne.b32 p, %5, 0;\n"
-        "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], bd, %4, p;\n"
-        "}\n" ::"r"(d_tmem),
-        "r"(a_tmem), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(accumulate)
-        : "memory");
-  } else {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        ".reg .b64 bd;\n"
-        "mov.b64 bd, {%2, %3};\n"
-        "setp.ne.b32 p, %5, 0;\n"
-        "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], bd, %4, p;\n"
-        "}\n" ::"r"(d_tmem),
-        "r"(a_tmem), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(accumulate)
-        : "memory");
-  }
-}
-
-// Warp-converged issue: the whole MMA warp runs the issue loop (warp-uniform
+// CTA-pair MMAs (M = 256 across the pair, issued by the leader CTA), in
+// warp-converged form: the whole MMA warp runs the issue loop (warp-uniform
 // descriptors, no per-instruction register -> uniform-register hand-off from a
 // divergent lane) and elect.sync picks the one lane that issues.
+// mma_pair_ts_el: A in tensor memory (each CTA's TMEM holds its 128 rows: lane =
+// row, column = 32-bit word of K), B from shared memory.
+// mma_pair_split_el: both operands from shared memory, each descriptor given as
+// (low, high) 32-bit halves.
 template <bool kTF32>
 __device__ __forceinline__ void mma_pair_ts_el(uint32_t d_tmem, uint32_t a_tmem, uint32_t b_lo,
                                                uint32_t b_hi, uint32_t idesc, uint32_t accumulate) {
@@ -541,21 +421,6 @@ __device__ __forceinline__ void regs_dec() {
 template <uint32_t kRegs>
 __device__ __forceinline__ void regs_inc() {
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegs));
-}
-
-// MN-major swizzled operand descriptor: atoms of 128-byte MN rows (8 rows for
-// SWIZZLE_128B, layout 2; 4 rows for SWIZZLE_128B_BASE32B, layout 1 -- the only
-// MN-major layout for 32-bit TF32 operands); LBO = byte stride between MN
-// atoms, SBO = byte stride between K row-groups.
-__device__ __forceinline__ uint64_t umma_desc_mnmajor(uint32_t smem_addr, uint32_t lbo,
-                                                      uint32_t sbo, uint32_t layout) {
-  uint64_t d = 0;
-  d |= static_cast<uint64_t>((smem_addr >> 4) & 0x3FFFu);
-  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
-  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
-  d |= static_cast<uint64_t>(1u) << 46;
-  d |= static_cast<uint64_t>(layout & 7u) << 61;
-  return d;
 }
 
 // Instruction descriptor with an MN-major B operand (bit 16).
